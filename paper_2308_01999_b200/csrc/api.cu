@@ -1,0 +1,1156 @@
+// api.cu — the C ABI (include/dsv.h): state handles, argument validation,
+// gate canonicalisation, kernel dispatch, instrumentation.
+//
+// Host-side responsibilities that the reference performs with NumPy index
+// gymnastics (statevec.py:26-60) are done here once per gate in O(2^k):
+//   * targets are sorted and the matrix / permutation re-indexed to the
+//     sorted order, so kernels see canonical geometry;
+//   * the control subcube + target positions become a Geom (hole insertion
+//     masks) and 2^k member offsets;
+//   * the access mode is chosen: complex64 with index bit 0 free runs on
+//     128-bit float4 units holding two amplitudes.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dsv.h"
+#include "common.cuh"
+#include "launch.h"
+
+using namespace dsv;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return fail(DSV_ENOMEM, "%s: out of device memory (%s)", what, cudaGetErrorString(e));
+  return fail(DSV_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr)                                         \
+  do {                                                   \
+    cudaError_t e_ = (expr);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);  \
+  } while (0)
+
+#define CKL(expr, n)                                     \
+  do {                                                   \
+    cudaError_t e_ = (expr);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);  \
+    g_launches += (n);                                   \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+enum ProfClass {
+  PC_DENSE = 0, PC_DENSE_GENERIC, PC_PERM, PC_PERM_GENERIC, PC_SWAP, PC_REDUCE,
+  PC_EXPECT, PC_PAULI, PC_COLLAPSE, PC_EXCHANGE, PC_ACCESS, PC_SAMPLE
+};
+const char* kProfNames[DSV_PROF_NCLASS] = {
+    "dense", "dense_generic", "genperm", "genperm_generic", "swap_bits", "reduce",
+    "expect", "pauli", "collapse", "exchange", "access", "sample"};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+}  // namespace
+
+struct dsv_state {
+  int device = 0;
+  int nbits = 0;
+  int dtype = 0;
+  void* d = nullptr;
+  bool owned = true;
+  bool ipc = false;
+  cudaStream_t stream = nullptr;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  bool prof_on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t uev[16] = {};
+};
+
+namespace {
+
+size_t amp_bytes(int dtype) { return dtype == DSV_C128 ? 16 : 8; }
+uint64_t namps(const dsv_state* s) { return 1ull << s->nbits; }
+
+int ensure_scratch(dsv_state* s, size_t bytes) {
+  if (s->scratch_bytes >= bytes) return DSV_OK;
+  if (s->scratch) {
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaFree(s->scratch));
+    s->scratch = nullptr;
+    s->scratch_bytes = 0;
+  }
+  size_t want = std::max<size_t>(bytes, size_t(1) << 20);
+  CK(cudaMalloc(&s->scratch, want));
+  s->scratch_bytes = want;
+  return DSV_OK;
+}
+
+cudaEvent_t pool_event(dsv_state* s) {
+  if (!s->ev_pool.empty()) {
+    cudaEvent_t e = s->ev_pool.back();
+    s->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfTok {
+  cudaEvent_t a = nullptr;
+};
+
+ProfTok prof_start(dsv_state* s) {
+  ProfTok t;
+  if (s->prof_on) {
+    t.a = pool_event(s);
+    cudaEventRecord(t.a, s->stream);
+  }
+  return t;
+}
+
+void prof_stop(dsv_state* s, ProfTok t, int cls, double bytes) {
+  if (!s->prof_on || !t.a) return;
+  cudaEvent_t b = pool_event(s);
+  cudaEventRecord(b, s->stream);
+  s->recs.push_back(ProfRec{cls, t.a, b, bytes});
+}
+
+int check_state(const dsv_state* s) {
+  if (!s) return fail(DSV_EINVAL, "null state");
+  return DSV_OK;
+}
+
+// Geometry over a unit index space of `ubits` bits with sorted holes.
+int make_geom(int ubits, const std::vector<int>& holes_sorted, uint64_t set_mask, Geom* g) {
+  const int H = int(holes_sorted.size());
+  if (H > ubits) return fail(DSV_EINVAL, "more hole bits (%d) than index bits (%d)", H, ubits);
+  if (H + 1 > DSV_MAX_GEOM_SEGS) return fail(DSV_EUNSUPPORTED, "too many hole bits");
+  std::memset(g, 0, sizeof(Geom));
+  g->nwork = 1ull << (ubits - H);
+  g->set_mask = set_mask;
+  g->nseg = H + 1;
+  for (int i = 0; i <= H; ++i) {
+    const int lo = i == 0 ? 0 : holes_sorted[i - 1] + 1;
+    const int hi = i == H ? 64 : holes_sorted[i];
+    uint64_t m = 0;
+    for (int b = lo; b < hi; ++b) m |= 1ull << b;
+    g->seg[i] = m;
+  }
+  return DSV_OK;
+}
+
+struct GateGeom {
+  int k = 0, nctrl = 0;
+  std::vector<int> tsorted;  // sorted targets (amp bits)
+  std::vector<int> order;    // order[m'] = original target position of sorted m'
+  std::vector<int> holes;    // sorted targets + control bits (amp bits)
+  uint64_t set_mask = 0;     // amp space
+};
+
+int validate_gate(const dsv_state* s, const int32_t* targets, int k, const int32_t* cb,
+                  const int32_t* cv, int nctrl, GateGeom* gg) {
+  if (k < 0 || k > DSV_MAX_TARGETS)
+    return fail(DSV_EINVAL, "gate arity %d outside [0, %d]", k, DSV_MAX_TARGETS);
+  if (nctrl < 0) return fail(DSV_EINVAL, "negative control count");
+  if (k > 0 && !targets) return fail(DSV_EINVAL, "null targets");
+  if (nctrl > 0 && (!cb || !cv)) return fail(DSV_EINVAL, "null controls");
+  uint64_t seen = 0;
+  for (int m = 0; m < k; ++m) {
+    const int t = targets[m];
+    if (t < 0 || t >= s->nbits) return fail(DSV_EINVAL, "target bit %d out of range [0, %d)", t, s->nbits);
+    if (seen >> t & 1) return fail(DSV_EINVAL, "duplicate bit %d", t);
+    seen |= 1ull << t;
+  }
+  gg->set_mask = 0;
+  for (int c = 0; c < nctrl; ++c) {
+    const int b = cb[c];
+    if (b < 0 || b >= s->nbits) return fail(DSV_EINVAL, "control bit %d out of range [0, %d)", b, s->nbits);
+    if (seen >> b & 1) return fail(DSV_EINVAL, "targets/controls overlap at bit %d", b);
+    if (cv[c] != 0 && cv[c] != 1) return fail(DSV_EINVAL, "control value %d not in {0,1}", cv[c]);
+    seen |= 1ull << b;
+    if (cv[c]) gg->set_mask |= 1ull << b;
+  }
+  gg->k = k;
+  gg->nctrl = nctrl;
+  gg->order.resize(k);
+  for (int m = 0; m < k; ++m) gg->order[m] = m;
+  std::sort(gg->order.begin(), gg->order.end(),
+            [&](int x, int y) { return targets[x] < targets[y]; });
+  gg->tsorted.resize(k);
+  for (int m = 0; m < k; ++m) gg->tsorted[m] = targets[gg->order[m]];
+  gg->holes.clear();
+  for (int b = 0; b < 64; ++b)
+    if (seen >> b & 1) gg->holes.push_back(b);
+  return DSV_OK;
+}
+
+// index j' in sorted-target order -> index j in caller order
+inline uint64_t old_index(const GateGeom& gg, uint64_t jn) {
+  uint64_t j = 0;
+  for (int m = 0; m < gg.k; ++m) j |= ((jn >> m) & 1ull) << gg.order[m];
+  return j;
+}
+inline uint64_t new_index(const GateGeom& gg, uint64_t j) {
+  uint64_t jn = 0;
+  for (int m = 0; m < gg.k; ++m) jn |= ((j >> gg.order[m]) & 1ull) << m;
+  return jn;
+}
+
+// unit-space view of a gate: VEC2 when complex64 and index bit 0 is not a hole
+struct UnitView {
+  int mode;
+  int ubits;
+  int shift;
+  Geom g;
+  std::vector<uint64_t> offs;  // 2^k member offsets (units)
+};
+
+int unit_view(const dsv_state* s, const GateGeom& gg, bool allow_vec2, UnitView* uv) {
+  const bool bit0_hole = !gg.holes.empty() && gg.holes[0] == 0;
+  uv->mode = (s->dtype == DSV_C64 && allow_vec2 && !bit0_hole && s->nbits >= 1) ? MODE_VEC2 : MODE_SCALAR;
+  uv->shift = uv->mode == MODE_VEC2 ? 1 : 0;
+  uv->ubits = s->nbits - uv->shift;
+  std::vector<int> h(gg.holes);
+  for (int& x : h) x -= uv->shift;
+  int rc = make_geom(uv->ubits, h, gg.set_mask >> uv->shift, &uv->g);
+  if (rc) return rc;
+  const uint64_t D = 1ull << gg.k;
+  uv->offs.assign(D, 0);
+  for (uint64_t j = 0; j < D; ++j) {
+    uint64_t o = 0;
+    for (int m = 0; m < gg.k; ++m) o |= ((j >> m) & 1ull) << (gg.tsorted[m] - uv->shift);
+    uv->offs[j] = o;
+  }
+  return DSV_OK;
+}
+
+template <typename R>
+void canon_matrix(const GateGeom& gg, const void* m_in, std::vector<cplx<R>>& out) {
+  const uint64_t D = 1ull << gg.k;
+  const cplx<R>* m = static_cast<const cplx<R>*>(m_in);
+  std::vector<uint64_t> old(D);
+  for (uint64_t j = 0; j < D; ++j) old[j] = old_index(gg, j);
+  out.resize(D * D);
+  for (uint64_t r = 0; r < D; ++r)
+    for (uint64_t c = 0; c < D; ++c) out[r * D + c] = m[old[r] * D + old[c]];
+}
+
+int sync_streams(dsv_state* waiter, dsv_state* other) {
+  if (waiter->stream == other->stream) return DSV_OK;
+  cudaEvent_t e;
+  {
+    DeviceGuard g(other->device);
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, other->stream));
+  }
+  CK(cudaStreamWaitEvent(waiter->stream, e, 0));
+  cudaEventDestroy(e);
+  return DSV_OK;
+}
+
+std::mutex g_peer_mu;
+bool g_peer_enabled[64][64];
+
+int enable_peer(int from, int to) {
+  if (from == to) return DSV_OK;
+  std::lock_guard<std::mutex> lk(g_peer_mu);
+  if (g_peer_enabled[from][to]) return DSV_OK;
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, from, to));
+  if (!can) return fail(DSV_EUNSUPPORTED, "device %d cannot access peer %d", from, to);
+  DeviceGuard g(from);
+  cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  cudaGetLastError();
+  g_peer_enabled[from][to] = true;
+  return DSV_OK;
+}
+
+// reduce partials already on device -> host doubles
+int finish_reduce(dsv_state* s, uint64_t nbins, uint64_t nchunks, int ncomp, double* d_partial,
+                  double* d_out, double* host_out) {
+  CKL(launch_final_sum(nbins, nchunks, ncomp, d_partial, d_out, s->stream), 1);
+  CK(cudaMemcpyAsync(host_out, d_out, sizeof(double) * nbins * ncomp, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+struct PauliMasks {
+  uint64_t x = 0, yz = 0;
+  int ny = 0, h = -1;
+};
+
+int parse_pauli(const dsv_state* s, const int32_t* bits, const char* paulis, int m, PauliMasks* pm) {
+  if (m < 0) return fail(DSV_EINVAL, "negative Pauli length");
+  uint64_t seen = 0;
+  for (int i = 0; i < m; ++i) {
+    const int b = bits[i];
+    if (b < 0 || b >= s->nbits) return fail(DSV_EINVAL, "Pauli bit %d out of range [0, %d)", b, s->nbits);
+    if (seen >> b & 1) return fail(DSV_EINVAL, "duplicate qubit in Pauli string: bit %d", b);
+    seen |= 1ull << b;
+    switch (paulis[i]) {
+      case 'I': case 'i': break;
+      case 'X': case 'x': pm->x |= 1ull << b; break;
+      case 'Y': case 'y': pm->x |= 1ull << b; pm->yz |= 1ull << b; pm->ny++; break;
+      case 'Z': case 'z': pm->yz |= 1ull << b; break;
+      default: return fail(DSV_EINVAL, "unknown Pauli factor '%c'", paulis[i]);
+    }
+  }
+  pm->h = -1;
+  for (int b = 63; b >= 0; --b)
+    if (pm->x >> b & 1) { pm->h = b; break; }
+  return DSV_OK;
+}
+
+// (-i)^ny
+void minus_i_pow(int ny, double* re, double* im) {
+  static const double t[4][2] = {{1, 0}, {0, -1}, {-1, 0}, {0, 1}};
+  *re = t[ny & 3][0];
+  *im = t[ny & 3][1];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dsv_last_error(void) { return g_err.c_str(); }
+int dsv_version(void) { return 1; }
+
+int dsv_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *out = n;
+  return DSV_OK;
+}
+
+int dsv_launch_count(uint64_t* out) {
+  *out = g_launches.load();
+  return DSV_OK;
+}
+
+int dsv_state_create(int device, int nbits, int dtype, dsv_state** out) {
+  if (!out) return fail(DSV_EINVAL, "null out");
+  *out = nullptr;
+  if (nbits < 0 || nbits > DSV_MAX_BITS) return fail(DSV_EINVAL, "nbits %d outside [0, %d]", nbits, DSV_MAX_BITS);
+  if (dtype != DSV_C64 && dtype != DSV_C128) return fail(DSV_EINVAL, "dtype %d not c64/c128", dtype);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(DSV_EINVAL, "device %d outside [0, %d)", device, ndev);
+  DeviceGuard g(device);
+  dsv_state* s = new dsv_state;
+  s->device = device;
+  s->nbits = nbits;
+  s->dtype = dtype;
+  const size_t bytes = amp_bytes(dtype) << nbits;
+  cudaError_t e = cudaMalloc(&s->d, bytes);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_fail(e, "cudaMalloc(state)");
+  }
+  e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaFree(s->d);
+    delete s;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = s;
+  return dsv_set_basis(s, 0);
+}
+
+int dsv_state_destroy(dsv_state* s) {
+  if (!s) return DSV_OK;
+  DeviceGuard g(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto& r : s->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : s->ev_pool) cudaEventDestroy(e);
+  for (auto e : s->uev)
+    if (e) cudaEventDestroy(e);
+  if (s->scratch) cudaFree(s->scratch);
+  if (s->d) {
+    if (s->ipc) cudaIpcCloseMemHandle(s->d);
+    else if (s->owned) cudaFree(s->d);
+  }
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return DSV_OK;
+}
+
+int dsv_state_info(const dsv_state* s, int* device, int* nbits, int* dtype) {
+  if (int rc = check_state(s)) return rc;
+  if (device) *device = s->device;
+  if (nbits) *nbits = s->nbits;
+  if (dtype) *dtype = s->dtype;
+  return DSV_OK;
+}
+
+int dsv_state_device_ptr(const dsv_state* s, void** out) {
+  if (int rc = check_state(s)) return rc;
+  *out = s->d;
+  return DSV_OK;
+}
+
+int dsv_sync(dsv_state* s) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+int dsv_set_zero(dsv_state* s) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  CK(cudaMemsetAsync(s->d, 0, amp_bytes(s->dtype) << s->nbits, s->stream));
+  return DSV_OK;
+}
+
+int dsv_set_basis(dsv_state* s, uint64_t index) {
+  if (int rc = check_state(s)) return rc;
+  if (index >= namps(s)) return fail(DSV_EINVAL, "basis index out of range");
+  DeviceGuard g(s->device);
+  CK(cudaMemsetAsync(s->d, 0, amp_bytes(s->dtype) << s->nbits, s->stream));
+  if (s->dtype == DSV_C128) {
+    static const double one[2] = {1.0, 0.0};
+    CK(cudaMemcpyAsync(static_cast<char*>(s->d) + 16 * index, one, 16, cudaMemcpyHostToDevice, s->stream));
+  } else {
+    static const float one[2] = {1.0f, 0.0f};
+    CK(cudaMemcpyAsync(static_cast<char*>(s->d) + 8 * index, one, 8, cudaMemcpyHostToDevice, s->stream));
+  }
+  return DSV_OK;
+}
+
+int dsv_upload(dsv_state* s, uint64_t begin, uint64_t count, const void* host) {
+  if (int rc = check_state(s)) return rc;
+  if (begin > namps(s) || count > namps(s) - begin) return fail(DSV_EINVAL, "upload range exceeds state");
+  if (count == 0) return DSV_OK;
+  DeviceGuard g(s->device);
+  const size_t ab = amp_bytes(s->dtype);
+  CK(cudaMemcpyAsync(static_cast<char*>(s->d) + ab * begin, host, ab * count, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+int dsv_download(dsv_state* s, uint64_t begin, uint64_t count, void* host) {
+  if (int rc = check_state(s)) return rc;
+  if (begin > namps(s) || count > namps(s) - begin) return fail(DSV_EINVAL, "download range exceeds state");
+  if (count == 0) return DSV_OK;
+  DeviceGuard g(s->device);
+  const size_t ab = amp_bytes(s->dtype);
+  CK(cudaMemcpyAsync(host, static_cast<const char*>(s->d) + ab * begin, ab * count, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+int dsv_copy(dsv_state* dst, const dsv_state* src) {
+  if (int rc = check_state(dst)) return rc;
+  if (int rc = check_state(src)) return rc;
+  if (dst->nbits != src->nbits || dst->dtype != src->dtype) return fail(DSV_EINVAL, "copy between states of different shape");
+  DeviceGuard g(dst->device);
+  if (int rc = sync_streams(dst, const_cast<dsv_state*>(src))) return rc;
+  const size_t bytes = amp_bytes(dst->dtype) << dst->nbits;
+  if (dst->device == src->device)
+    CK(cudaMemcpyAsync(dst->d, src->d, bytes, cudaMemcpyDeviceToDevice, dst->stream));
+  else
+    CK(cudaMemcpyPeerAsync(dst->d, dst->device, src->d, src->device, bytes, dst->stream));
+  return sync_streams(const_cast<dsv_state*>(src), dst);
+}
+
+// ---- gates -----------------------------------------------------------------------------
+
+int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, int k,
+                     const int32_t* cb, const int32_t* cv, int nctrl) {
+  if (int rc = check_state(s)) return rc;
+  if (!matrix) return fail(DSV_EINVAL, "null matrix");
+  GateGeom gg;
+  if (int rc = validate_gate(s, targets, k, cb, cv, nctrl, &gg)) return rc;
+  DeviceGuard g(s->device);
+  const double bytes = 2.0 * double(amp_bytes(s->dtype)) * std::ldexp(1.0, s->nbits - nctrl);
+  const uint64_t D = 1ull << k;
+  if (k <= kDenseRegMaxK) {
+    UnitView uv;
+    // float4 pairs only while 2^k x 2 amplitudes fit the register budget
+    if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;
+    ProfTok t = prof_start(s);
+    if (s->dtype == DSV_C128) {
+      std::vector<cplx<double>> m;
+      canon_matrix<double>(gg, matrix, m);
+      CKL(launch_dense_reg(s->dtype, uv.mode, k, uv.g, uv.offs.data(), m.data(), s->d, s->stream), 1);
+    } else {
+      std::vector<cplx<float>> m;
+      canon_matrix<float>(gg, matrix, m);
+      CKL(launch_dense_reg(s->dtype, uv.mode, k, uv.g, uv.offs.data(), m.data(), s->d, s->stream), 1);
+    }
+    prof_stop(s, t, PC_DENSE, bytes);
+    return DSV_OK;
+  }
+  // generic path (k = 6..10): offsets + transposed matrix staged in device scratch
+  UnitView uv;
+  if (int rc = unit_view(s, gg, false, &uv)) return rc;
+  const size_t ab = amp_bytes(s->dtype);
+  const size_t off_bytes = D * sizeof(uint64_t);
+  const size_t mat_bytes = D * D * ab;
+  if (int rc = ensure_scratch(s, off_bytes + mat_bytes + 256)) return rc;
+  std::vector<unsigned char> mt(mat_bytes);
+  if (s->dtype == DSV_C128) {
+    std::vector<cplx<double>> m;
+    canon_matrix<double>(gg, matrix, m);
+    cplx<double>* o = reinterpret_cast<cplx<double>*>(mt.data());
+    for (uint64_t r = 0; r < D; ++r)
+      for (uint64_t c = 0; c < D; ++c) o[c * D + r] = m[r * D + c];
+  } else {
+    std::vector<cplx<float>> m;
+    canon_matrix<float>(gg, matrix, m);
+    cplx<float>* o = reinterpret_cast<cplx<float>*>(mt.data());
+    for (uint64_t r = 0; r < D; ++r)
+      for (uint64_t c = 0; c < D; ++c) o[c * D + r] = m[r * D + c];
+  }
+  char* base = static_cast<char*>(s->scratch);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(base);
+  void* d_mt = base + ((off_bytes + 255) / 256) * 256;
+  CK(cudaMemcpyAsync(d_offs, uv.offs.data(), off_bytes, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(d_mt, mt.data(), mat_bytes, cudaMemcpyHostToDevice, s->stream));
+  ProfTok t = prof_start(s);
+  CKL(launch_dense_generic(s->dtype, k, uv.g, d_offs, d_mt, s->d, s->stream), 1);
+  prof_stop(s, t, PC_DENSE_GENERIC, bytes);
+  // the host staging vectors die at return: make the copies complete first
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const int32_t* targets,
+                      int k, const int32_t* cb, const int32_t* cv, int nctrl) {
+  if (int rc = check_state(s)) return rc;
+  if (!perm || !diag) return fail(DSV_EINVAL, "null permutation/diagonal");
+  GateGeom gg;
+  if (int rc = validate_gate(s, targets, k, cb, cv, nctrl, &gg)) return rc;
+  const uint64_t D = 1ull << k;
+  {
+    std::vector<char> hit(D, 0);
+    for (uint64_t j = 0; j < D; ++j) {
+      if (perm[j] < 0 || uint64_t(perm[j]) >= D || hit[perm[j]])
+        return fail(DSV_EINVAL, "permutation table is not a bijection");
+      hit[perm[j]] = 1;
+    }
+  }
+  DeviceGuard g(s->device);
+  // canonical tables: perm'[j'] = new(perm[old(j')]), diag'[j'] = diag[old(j')]
+  std::vector<uint64_t> pn(D);
+  std::vector<unsigned char> dn(D * amp_bytes(s->dtype));
+  uint64_t nactive = 0;
+  std::vector<char> act(D, 0);
+  for (uint64_t jn = 0; jn < D; ++jn) {
+    const uint64_t j = old_index(gg, jn);
+    pn[jn] = new_index(gg, uint64_t(perm[j]));
+    bool unit;
+    if (s->dtype == DSV_C128) {
+      const cplx<double> v = static_cast<const cplx<double>*>(diag)[j];
+      reinterpret_cast<cplx<double>*>(dn.data())[jn] = v;
+      unit = v.x == 1.0 && v.y == 0.0;
+    } else {
+      const cplx<float> v = static_cast<const cplx<float>*>(diag)[j];
+      reinterpret_cast<cplx<float>*>(dn.data())[jn] = v;
+      unit = v.x == 1.0f && v.y == 0.0f;
+    }
+    act[jn] = !(pn[jn] == jn && unit);
+    nactive += act[jn];
+  }
+  if (nactive == 0) return DSV_OK;  // identity table: nothing moves (bit-exact no-op)
+  const double bytes = 2.0 * double(amp_bytes(s->dtype)) * std::ldexp(1.0, s->nbits - nctrl) *
+                       double(nactive) / double(D);
+  bool is_diag = true;
+  for (uint64_t j = 0; j < D; ++j) is_diag = is_diag && pn[j] == j;
+  if (is_diag) {
+    // elementwise path: holes = control bits only, targets stay in the stream
+    GateGeom cg = gg;
+    cg.holes.clear();
+    for (int c = 0; c < nctrl; ++c) cg.holes.push_back(cb[c]);
+    std::sort(cg.holes.begin(), cg.holes.end());
+    const bool bit0_used = (!gg.tsorted.empty() && gg.tsorted[0] == 0) || (!cg.holes.empty() && cg.holes[0] == 0);
+    const bool vec2 = s->dtype == DSV_C64 && !bit0_used && s->nbits >= 1;
+    const int sh = vec2 ? 1 : 0;
+    std::vector<int> h(cg.holes);
+    for (int& x : h) x -= sh;
+    Geom geo;
+    if (int rc = make_geom(s->nbits - sh, h, gg.set_mask >> sh, &geo)) return rc;
+    int tb[DSV_MAX_TARGETS];
+    for (int m = 0; m < k; ++m) tb[m] = gg.tsorted[m] - sh;
+    std::vector<unsigned char> av(D);
+    for (uint64_t j = 0; j < D; ++j) av[j] = act[j];
+    ProfTok t = prof_start(s);
+    CKL(launch_diag(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, k, geo, tb, dn.data(), av.data(), s->d, s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
+  if (k <= kPermRegMaxK) {
+    UnitView uv;
+    if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;
+    std::vector<uint64_t> oo(D);
+    uint64_t active = 0;
+    for (uint64_t j = 0; j < D; ++j) {
+      oo[j] = uv.offs[pn[j]];
+      if (act[j]) active |= 1ull << j;
+    }
+    ProfTok t = prof_start(s);
+    CKL(launch_perm_reg(s->dtype, uv.mode, k, uv.g, uv.offs.data(), oo.data(), dn.data(), active, s->d, s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
+  UnitView uv;
+  if (int rc = unit_view(s, gg, false, &uv)) return rc;
+  std::vector<uint64_t> oo(D);
+  for (uint64_t j = 0; j < D; ++j) oo[j] = uv.offs[pn[j]];
+  const size_t ob = D * sizeof(uint64_t);
+  const size_t obr = ((ob + 255) / 256) * 256;
+  if (int rc = ensure_scratch(s, 2 * obr + dn.size() + 256)) return rc;
+  char* base = static_cast<char*>(s->scratch);
+  CK(cudaMemcpyAsync(base, uv.offs.data(), ob, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(base + obr, oo.data(), ob, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(base + 2 * obr, dn.data(), dn.size(), cudaMemcpyHostToDevice, s->stream));
+  ProfTok t = prof_start(s);
+  CKL(launch_perm_generic(s->dtype, k, uv.g, reinterpret_cast<uint64_t*>(base),
+                          reinterpret_cast<uint64_t*>(base + obr), base + 2 * obr, s->d, s->stream), 1);
+  prof_stop(s, t, PC_PERM_GENERIC, bytes);
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+int dsv_apply_pauli_rotation(dsv_state* s, double theta, double coef_re, double coef_im,
+                             const int32_t* bits, const char* paulis, int m) {
+  if (int rc = check_state(s)) return rc;
+  PauliMasks pm;
+  if (int rc = parse_pauli(s, bits, paulis, m, &pm)) return rc;
+  DeviceGuard g(s->device);
+  double pr, pi;
+  minus_i_pow(pm.ny, &pr, &pi);
+  const double sn = std::sin(theta / 2), cs = std::cos(theta / 2);
+  // B = -i * sin * coef * (-i)^ny
+  const double cr = coef_re * pr - coef_im * pi, ci = coef_re * pi + coef_im * pr;
+  PauliOp op;
+  op.xmask = pm.x;
+  op.yzmask = pm.yz;
+  op.hbit = pm.h;
+  op.c = cs;
+  op.br = sn * ci;
+  op.bi = -sn * cr;
+  ProfTok t = prof_start(s);
+  CKL(launch_pauli(s->dtype, s->nbits, op, s->d, s->stream), 1);
+  prof_stop(s, t, PC_PAULI, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  return DSV_OK;
+}
+
+int dsv_apply_pauli_product(dsv_state* s, const int32_t* bits, const char* paulis, int m) {
+  if (int rc = check_state(s)) return rc;
+  PauliMasks pm;
+  if (int rc = parse_pauli(s, bits, paulis, m, &pm)) return rc;
+  if (pm.x == 0 && pm.yz == 0) return DSV_OK;
+  DeviceGuard g(s->device);
+  PauliOp op;
+  op.xmask = pm.x;
+  op.yzmask = pm.yz;
+  op.hbit = pm.h;
+  op.c = 0.0;
+  minus_i_pow(pm.ny, &op.br, &op.bi);
+  ProfTok t = prof_start(s);
+  CKL(launch_pauli(s->dtype, s->nbits, op, s->d, s->stream), 1);
+  prof_stop(s, t, PC_PAULI, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  return DSV_OK;
+}
+
+// ---- layout -----------------------------------------------------------------------------
+
+int dsv_swap_index_bits(dsv_state* s, const int32_t* pairs, int npairs) {
+  if (int rc = check_state(s)) return rc;
+  if (npairs < 0) return fail(DSV_EINVAL, "negative pair count");
+  uint64_t seen = 0;
+  SwapPairs sp;
+  sp.np = 0;
+  bool bit0 = false;
+  for (int q = 0; q < npairs; ++q) {
+    const int a = pairs[2 * q], b = pairs[2 * q + 1];
+    if (a < 0 || a >= s->nbits || b < 0 || b >= s->nbits)
+      return fail(DSV_EINVAL, "bit pair (%d, %d) exceeds %d qubits", a, b, s->nbits);
+    if ((seen >> a & 1) || (seen >> b & 1) || (a == b && false))
+      return fail(DSV_EINVAL, "bit appears in more than one pair");
+    seen |= 1ull << a;
+    seen |= 1ull << b;
+    if (a == b) continue;
+    if (sp.np >= 20) return fail(DSV_EUNSUPPORTED, "more than 20 swap pairs");
+    sp.a[sp.np] = a;
+    sp.b[sp.np] = b;
+    sp.np++;
+    if (a == 0 || b == 0) bit0 = true;
+  }
+  if (sp.np == 0) return DSV_OK;
+  DeviceGuard g(s->device);
+  int mode = MODE_SCALAR;
+  uint64_t nunits = namps(s);
+  if (s->dtype == DSV_C64 && !bit0) {
+    mode = MODE_VEC2;
+    nunits >>= 1;
+    for (int q = 0; q < sp.np; ++q) { sp.a[q] -= 1; sp.b[q] -= 1; }
+  }
+  const double bytes = 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)) * (1.0 - std::ldexp(1.0, -sp.np));
+  ProfTok t = prof_start(s);
+  CKL(launch_swap_bits(s->dtype, mode, nunits, sp, s->d, s->stream), 1);
+  prof_stop(s, t, PC_SWAP, bytes);
+  return DSV_OK;
+}
+
+static int check_ordering(const dsv_state* s, const int32_t* ordering) {
+  uint64_t seen = 0;
+  for (int b = 0; b < s->nbits; ++b) {
+    const int o = ordering[b];
+    if (o < 0 || o >= s->nbits || (seen >> o & 1))
+      return fail(DSV_EINVAL, "bit_ordering must be a permutation of all index bits");
+    seen |= 1ull << o;
+  }
+  return DSV_OK;
+}
+
+static const uint64_t kAccessChunk = 1ull << 25;
+
+int dsv_access_get(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64_t end, void* host_out) {
+  if (int rc = check_state(s)) return rc;
+  if (int rc = check_ordering(s, ordering)) return rc;
+  if (!(begin < end && end <= namps(s))) return fail(DSV_EINVAL, "bad range [%llu, %llu)",
+                                                     (unsigned long long)begin, (unsigned long long)end);
+  DeviceGuard g(s->device);
+  const size_t ab = amp_bytes(s->dtype);
+  const uint64_t chunk = std::min<uint64_t>(end - begin, kAccessChunk);
+  if (int rc = ensure_scratch(s, chunk * ab)) return rc;
+  for (uint64_t b0 = begin; b0 < end; b0 += chunk) {
+    const uint64_t cnt = std::min<uint64_t>(chunk, end - b0);
+    ProfTok t = prof_start(s);
+    CKL(launch_gather(s->dtype, s->nbits, ordering, b0, cnt, s->d, s->scratch, s->stream), 1);
+    prof_stop(s, t, PC_ACCESS, 2.0 * ab * cnt);
+    CK(cudaMemcpyAsync(static_cast<char*>(host_out) + (b0 - begin) * ab, s->scratch, cnt * ab,
+                       cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  return DSV_OK;
+}
+
+int dsv_access_set(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64_t count, const void* host_in) {
+  if (int rc = check_state(s)) return rc;
+  if (int rc = check_ordering(s, ordering)) return rc;
+  if (count == 0 || begin >= namps(s) || count > namps(s) - begin) return fail(DSV_EINVAL, "range exceeds state size");
+  DeviceGuard g(s->device);
+  const size_t ab = amp_bytes(s->dtype);
+  const uint64_t chunk = std::min<uint64_t>(count, kAccessChunk);
+  if (int rc = ensure_scratch(s, chunk * ab)) return rc;
+  for (uint64_t o = 0; o < count; o += chunk) {
+    const uint64_t cnt = std::min<uint64_t>(chunk, count - o);
+    CK(cudaMemcpyAsync(s->scratch, static_cast<const char*>(host_in) + o * ab, cnt * ab,
+                       cudaMemcpyHostToDevice, s->stream));
+    ProfTok t = prof_start(s);
+    CKL(launch_scatter(s->dtype, s->nbits, ordering, begin + o, cnt, s->d, s->scratch, s->stream), 1);
+    prof_stop(s, t, PC_ACCESS, 2.0 * ab * cnt);
+    CK(cudaStreamSynchronize(s->stream));
+  }
+  return DSV_OK;
+}
+
+// ---- reductions -----------------------------------------------------------------------------
+
+static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2, double* host_out,
+                      double** d_partial_out, uint64_t* nchunks_out) {
+  if (k < 0 || k > 26) return fail(DSV_EUNSUPPORTED, "marginal over %d bits not supported (max 26)", k);
+  uint64_t seen = 0;
+  for (int j = 0; j < k; ++j) {
+    const int b = bits[j];
+    if (b < 0 || b >= s->nbits) return fail(DSV_EINVAL, "qubit bit %d out of range", b);
+    if (seen >> b & 1) return fail(DSV_EINVAL, "qubits must be distinct");
+    seen |= 1ull << b;
+  }
+  const bool vec2 = allow_vec2 && s->dtype == DSV_C64 && !(seen & 1ull) && s->nbits >= 1;
+  const int shift = vec2 ? 1 : 0;
+  BinGeom bg;
+  std::memset(&bg, 0, sizeof bg);
+  std::vector<int> holes;
+  for (int b = 0; b < 64; ++b)
+    if (seen >> b & 1) holes.push_back(b - shift);
+  if (int rc = make_geom(s->nbits - shift, holes, 0, &bg.g)) return rc;
+  bg.nb = k;
+  for (int j = 0; j < k; ++j) bg.bits[j] = bits[j] - shift;
+  bg.nchunks = chunks_for(bg.g.nwork);
+  const uint64_t nbins = 1ull << k;
+  const size_t part_bytes = sizeof(double) * nbins * bg.nchunks;
+  const size_t part_round = ((part_bytes + 255) / 256) * 256;
+  if (int rc = ensure_scratch(s, part_round + sizeof(double) * nbins)) return rc;
+  double* d_partial = static_cast<double*>(s->scratch);
+  double* d_out = reinterpret_cast<double*>(static_cast<char*>(s->scratch) + part_round);
+  ProfTok t = prof_start(s);
+  CKL(launch_probs(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, bg, s->d, d_partial, s->stream), 1);
+  prof_stop(s, t, PC_REDUCE, double(amp_bytes(s->dtype)) * double(namps(s)));
+  if (d_partial_out) {
+    *d_partial_out = d_partial;
+    *nchunks_out = bg.nchunks;
+    return DSV_OK;
+  }
+  return finish_reduce(s, nbins, bg.nchunks, 1, d_partial, d_out, host_out);
+}
+
+int dsv_norm2(dsv_state* s, double* out) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  return probs_impl(s, nullptr, 0, true, out, nullptr, nullptr);
+}
+
+int dsv_marginal_probs(dsv_state* s, const int32_t* bits, int k, double* out) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  return probs_impl(s, bits, k, true, out, nullptr, nullptr);
+}
+
+int dsv_expect_pauli(dsv_state* s, const int32_t* bits, const char* paulis, int m, double* out) {
+  if (int rc = check_state(s)) return rc;
+  PauliMasks pm;
+  if (int rc = parse_pauli(s, bits, paulis, m, &pm)) return rc;
+  DeviceGuard g(s->device);
+  PauliOp op;
+  op.xmask = pm.x;
+  op.yzmask = pm.yz;
+  op.hbit = pm.h;
+  op.c = 0.0;
+  minus_i_pow(pm.ny, &op.br, &op.bi);
+  const uint64_t npairs = pm.h >= 0 ? namps(s) / 2 : namps(s);
+  const uint64_t nch = chunks_for(npairs);
+  const size_t pr = ((sizeof(double) * 2 * nch + 255) / 256) * 256;
+  if (int rc = ensure_scratch(s, pr + 16)) return rc;
+  double* d_partial = static_cast<double*>(s->scratch);
+  double* d_out = reinterpret_cast<double*>(static_cast<char*>(s->scratch) + pr);
+  uint64_t nchunks = 0;
+  ProfTok t = prof_start(s);
+  CKL(launch_expect_pauli(s->dtype, s->nbits, op, s->d, d_partial, &nchunks, s->stream), 1);
+  prof_stop(s, t, PC_EXPECT, double(amp_bytes(s->dtype)) * double(namps(s)));
+  return finish_reduce(s, 1, nchunks, 2, d_partial, d_out, out);
+}
+
+int dsv_inner(dsv_state* a, const dsv_state* b, double* out) {
+  if (int rc = check_state(a)) return rc;
+  if (int rc = check_state(b)) return rc;
+  if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "inner product of states with different shape");
+  DeviceGuard g(a->device);
+  if (a->device != b->device)
+    if (int rc = enable_peer(a->device, b->device)) return rc;
+  if (int rc = sync_streams(a, const_cast<dsv_state*>(b))) return rc;
+  const uint64_t nch = chunks_for(namps(a));
+  const size_t pr = ((sizeof(double) * 2 * nch + 255) / 256) * 256;
+  if (int rc = ensure_scratch(a, pr + 16)) return rc;
+  double* d_partial = static_cast<double*>(a->scratch);
+  double* d_out = reinterpret_cast<double*>(static_cast<char*>(a->scratch) + pr);
+  uint64_t nchunks = 0;
+  ProfTok t = prof_start(a);
+  CKL(launch_inner(a->dtype, namps(a), a->d, b->d, d_partial, &nchunks, a->stream), 1);
+  prof_stop(a, t, PC_EXPECT, 2.0 * double(amp_bytes(a->dtype)) * double(namps(a)));
+  return finish_reduce(a, 1, nchunks, 2, d_partial, d_out, out);
+}
+
+int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, int k, double* out) {
+  if (int rc = check_state(s)) return rc;
+  if (!matrix) return fail(DSV_EINVAL, "null matrix");
+  GateGeom gg;
+  if (int rc = validate_gate(s, targets, k, nullptr, nullptr, 0, &gg)) return rc;
+  DeviceGuard g(s->device);
+  if (k <= 4) {
+    UnitView uv;
+    if (int rc = unit_view(s, gg, false, &uv)) return rc;
+    const uint64_t maxch = 148ull * 8;
+    const size_t pr = ((sizeof(double) * 2 * maxch + 255) / 256) * 256;
+    if (int rc = ensure_scratch(s, pr + 16)) return rc;
+    double* d_partial = static_cast<double*>(s->scratch);
+    double* d_out = reinterpret_cast<double*>(static_cast<char*>(s->scratch) + pr);
+    uint64_t nchunks = 0;
+    ProfTok t = prof_start(s);
+    if (s->dtype == DSV_C128) {
+      std::vector<cplx<double>> m;
+      canon_matrix<double>(gg, matrix, m);
+      CKL(launch_expect_dense(s->dtype, k, uv.g, uv.offs.data(), m.data(), s->d, d_partial, &nchunks, s->stream), 1);
+    } else {
+      std::vector<cplx<float>> m;
+      canon_matrix<float>(gg, matrix, m);
+      CKL(launch_expect_dense(s->dtype, k, uv.g, uv.offs.data(), m.data(), s->d, d_partial, &nchunks, s->stream), 1);
+    }
+    prof_stop(s, t, PC_EXPECT, double(amp_bytes(s->dtype)) * double(namps(s)));
+    return finish_reduce(s, 1, nchunks, 2, d_partial, d_out, out);
+  }
+  // larger observables: copy, apply, <psi|work> (the reference's own algorithm)
+  dsv_state* work = nullptr;
+  if (int rc = dsv_state_create(s->device, s->nbits, s->dtype, &work)) return rc;
+  int rc = dsv_copy(work, s);
+  if (!rc) rc = dsv_apply_matrix(work, matrix, targets, k, nullptr, nullptr, 0);
+  if (!rc) rc = sync_streams(s, work);
+  if (!rc) rc = dsv_inner(s, work, out);
+  dsv_state_destroy(work);
+  return rc;
+}
+
+int dsv_collapse(dsv_state* s, const int32_t* bits, int k, uint64_t outcome, double norm2_kept) {
+  if (int rc = check_state(s)) return rc;
+  if (!(norm2_kept > 0.0)) return fail(DSV_EINVAL, "collapse onto a zero-probability outcome");
+  uint64_t mask = 0, val = 0;
+  for (int j = 0; j < k; ++j) {
+    const int b = bits[j];
+    if (b < 0 || b >= s->nbits) return fail(DSV_EINVAL, "qubit bit %d out of range", b);
+    if (mask >> b & 1) return fail(DSV_EINVAL, "qubits must be distinct");
+    mask |= 1ull << b;
+    val |= ((outcome >> j) & 1ull) << b;
+  }
+  DeviceGuard g(s->device);
+  const bool vec2 = s->dtype == DSV_C64 && !(mask & 1ull) && s->nbits >= 1;
+  const int sh = vec2 ? 1 : 0;
+  ProfTok t = prof_start(s);
+  CKL(launch_collapse(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, namps(s) >> sh, mask >> sh, val >> sh,
+                      1.0 / std::sqrt(norm2_kept), s->d, s->stream), 1);
+  prof_stop(s, t, PC_COLLAPSE, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  return DSV_OK;
+}
+
+int dsv_scale(dsv_state* s, double factor) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  const bool vec2 = s->dtype == DSV_C64 && s->nbits >= 1;
+  const int sh = vec2 ? 1 : 0;
+  ProfTok t = prof_start(s);
+  CKL(launch_collapse(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, namps(s) >> sh, 0, 0, factor, s->d, s->stream), 1);
+  prof_stop(s, t, PC_COLLAPSE, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  return DSV_OK;
+}
+
+int dsv_sample(dsv_state* s, const double* variates, int64_t shots, uint64_t* outcomes) {
+  if (int rc = check_state(s)) return rc;
+  if (shots < 1) return fail(DSV_EINVAL, "shots must be >= 1");
+  DeviceGuard g(s->device);
+  // 1) ordered chunk sums of |a|^2 over kChunk-amplitude chunks (scalar units)
+  double* d_partial = nullptr;
+  uint64_t nch = 0;
+  if (int rc = probs_impl(s, nullptr, 0, false, nullptr, &d_partial, &nch)) return rc;
+  const uint64_t chunk_amps = uint64_t(kReduceThreads) * kReduceUnitsPerThread;
+  std::vector<double> cs(nch);
+  CK(cudaMemcpyAsync(cs.data(), d_partial, sizeof(double) * nch, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  // 2) host prefix over chunks (sequential, float64)
+  std::vector<double> pre(nch);
+  double run = 0.0;
+  for (uint64_t c = 0; c < nch; ++c) {
+    run += cs[c];
+    pre[c] = run;
+  }
+  const double total = run;
+  if (!(total > 0.0)) return fail(DSV_EINVAL, "state has zero norm; cannot sample");
+  std::vector<uint64_t> ch(shots);
+  std::vector<double> rs(shots);
+  for (int64_t i = 0; i < shots; ++i) {
+    const double target = variates[i] * total;
+    uint64_t c = uint64_t(std::upper_bound(pre.begin(), pre.end(), target) - pre.begin());
+    if (c >= nch) c = nch - 1;
+    ch[i] = c;
+    rs[i] = target - (c ? pre[c - 1] : 0.0);
+  }
+  // 3) per-shot warp scan inside the chunk
+  const size_t b1 = ((sizeof(uint64_t) * shots + 255) / 256) * 256;
+  const size_t need = 3 * b1;
+  if (int rc = ensure_scratch(s, need)) return rc;
+  char* base = static_cast<char*>(s->scratch);
+  uint64_t* d_ch = reinterpret_cast<uint64_t*>(base);
+  double* d_rs = reinterpret_cast<double*>(base + b1);
+  uint64_t* d_out = reinterpret_cast<uint64_t*>(base + 2 * b1);
+  CK(cudaMemcpyAsync(d_ch, ch.data(), sizeof(uint64_t) * shots, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaMemcpyAsync(d_rs, rs.data(), sizeof(double) * shots, cudaMemcpyHostToDevice, s->stream));
+  ProfTok t = prof_start(s);
+  CKL(launch_sample_scan(s->dtype, namps(s), chunk_amps, shots, d_ch, d_rs, s->d, d_out, s->stream), 1);
+  prof_stop(s, t, PC_SAMPLE, double(amp_bytes(s->dtype)) * double(chunk_amps) * double(shots));
+  CK(cudaMemcpyAsync(outcomes, d_out, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+// ---- segments -----------------------------------------------------------------------------
+
+int dsv_exchange_halves(dsv_state* a, dsv_state* b, int local_bit, int part, int nparts) {
+  if (int rc = check_state(a)) return rc;
+  if (int rc = check_state(b)) return rc;
+  if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "exchange between segments of different shape");
+  if (local_bit < 0 || local_bit >= a->nbits) return fail(DSV_EINVAL, "local bit %d out of range", local_bit);
+  if (nparts < 1 || part < 0 || part >= nparts) return fail(DSV_EINVAL, "bad exchange slice %d/%d", part, nparts);
+  DeviceGuard g(a->device);
+  if (!b->ipc && a->device != b->device)
+    if (int rc = enable_peer(a->device, b->device)) return rc;
+  if (!b->ipc)
+    if (int rc = sync_streams(a, b)) return rc;
+  const bool vec2 = a->dtype == DSV_C64 && local_bit != 0;
+  const int sh = vec2 ? 1 : 0;
+  const uint64_t T = namps(a) >> (1 + sh);
+  const uint64_t lo = T / nparts * part + std::min<uint64_t>(part, T % nparts);
+  const uint64_t hi = lo + T / nparts + (uint64_t(part) < T % nparts ? 1 : 0);
+  ProfTok t = prof_start(a);
+  CKL(launch_exchange_halves(a->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, local_bit - sh, lo, hi, a->d, b->d, a->stream), 1);
+  prof_stop(a, t, PC_EXCHANGE, 4.0 * double(amp_bytes(a->dtype)) * double(hi - lo) * (vec2 ? 2.0 : 1.0));
+  if (!b->ipc)
+    if (int rc = sync_streams(b, a)) return rc;
+  return DSV_OK;
+}
+
+int dsv_exchange_all(dsv_state* a, dsv_state* b) {
+  if (int rc = check_state(a)) return rc;
+  if (int rc = check_state(b)) return rc;
+  if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "exchange between segments of different shape");
+  DeviceGuard g(a->device);
+  if (!b->ipc && a->device != b->device)
+    if (int rc = enable_peer(a->device, b->device)) return rc;
+  if (!b->ipc)
+    if (int rc = sync_streams(a, b)) return rc;
+  ProfTok t = prof_start(a);
+  CKL(launch_exchange_all(a->dtype, namps(a), a->d, b->d, a->stream), 1);
+  prof_stop(a, t, PC_EXCHANGE, 4.0 * double(amp_bytes(a->dtype)) * double(namps(a)));
+  if (!b->ipc)
+    if (int rc = sync_streams(b, a)) return rc;
+  return DSV_OK;
+}
+
+int dsv_ipc_handle(dsv_state* s, void* out64) {
+  if (int rc = check_state(s)) return rc;
+  if (s->ipc) return fail(DSV_EINVAL, "cannot re-export a peer mapping");
+  DeviceGuard g(s->device);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, s->d));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(out64, &h, 64);
+  return DSV_OK;
+}
+
+int dsv_peer_open(int device, int nbits, int dtype, const void* handle64, dsv_state** out) {
+  if (!out || !handle64) return fail(DSV_EINVAL, "null argument");
+  *out = nullptr;
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  dsv_state* s = new dsv_state;
+  s->device = device;
+  s->nbits = nbits;
+  s->dtype = dtype;
+  s->owned = false;
+  s->ipc = true;
+  cudaError_t e = cudaIpcOpenMemHandle(&s->d, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    delete s;
+    return cuda_fail(e, "cudaIpcOpenMemHandle");
+  }
+  e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaIpcCloseMemHandle(s->d);
+    delete s;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  *out = s;
+  return DSV_OK;
+}
+
+// ---- instrumentation ---------------------------------------------------------------------
+
+int dsv_prof_enable(dsv_state* s, int on) {
+  if (int rc = check_state(s)) return rc;
+  s->prof_on = on != 0;
+  return DSV_OK;
+}
+
+int dsv_prof_reset(dsv_state* s) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  CK(cudaStreamSynchronize(s->stream));
+  for (auto& r : s->recs) {
+    s->ev_pool.push_back(r.a);
+    s->ev_pool.push_back(r.b);
+  }
+  s->recs.clear();
+  return DSV_OK;
+}
+
+int dsv_prof_read(dsv_state* s, uint64_t* count, double* ms, double* bytes) {
+  if (int rc = check_state(s)) return rc;
+  DeviceGuard g(s->device);
+  CK(cudaStreamSynchronize(s->stream));
+  for (int c = 0; c < DSV_PROF_NCLASS; ++c) {
+    count[c] = 0;
+    ms[c] = 0.0;
+    bytes[c] = 0.0;
+  }
+  for (auto& r : s->recs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    count[r.cls] += 1;
+    ms[r.cls] += t;
+    bytes[r.cls] += r.bytes;
+  }
+  return DSV_OK;
+}
+
+const char* dsv_prof_class_name(int c) {
+  if (c < 0 || c >= DSV_PROF_NCLASS) return "";
+  return kProfNames[c];
+}
+
+int dsv_event_record(dsv_state* s, int slot) {
+  if (int rc = check_state(s)) return rc;
+  if (slot < 0 || slot >= 16) return fail(DSV_EINVAL, "event slot out of range");
+  DeviceGuard g(s->device);
+  if (!s->uev[slot]) CK(cudaEventCreate(&s->uev[slot]));
+  CK(cudaEventRecord(s->uev[slot], s->stream));
+  return DSV_OK;
+}
+
+int dsv_event_elapsed(dsv_state* s, int a, int b, float* ms) {
+  if (int rc = check_state(s)) return rc;
+  if (a < 0 || a >= 16 || b < 0 || b >= 16 || !s->uev[a] || !s->uev[b]) return fail(DSV_EINVAL, "event slot not recorded");
+  DeviceGuard g(s->device);
+  CK(cudaEventSynchronize(s->uev[b]));
+  CK(cudaEventElapsedTime(ms, s->uev[a], s->uev[b]));
+  return DSV_OK;
+}
+
+}  // extern "C"

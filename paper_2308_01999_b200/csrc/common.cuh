@@ -1,0 +1,106 @@
+// common.cuh — shared device-side machinery for the dsv kernels (sm_100a).
+//
+// Index geometry.  Every gate / reduction kernel enumerates "work items":
+// the 2^(n-H) assignments of the index bits that are NOT holes (holes =
+// target bits + control bits, or the bits a reduction bins over).  A work
+// item w is expanded to the base index of its amplitude group by inserting
+// zeros at the hole positions, then OR-ing the control values — the
+// device-side equivalent of the reference's `_controlled_subview` +
+// `np.moveaxis` gather (statevec.py:26-41, :56-59), without materialising
+// anything.  Consecutive threads take consecutive work items, so the lowest
+// free bits vary fastest and HBM accesses coalesce whenever the low index
+// bits are free.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define DSV_MAX_GEOM_SEGS 41  // DSV_MAX_BITS holes + 1
+
+namespace dsv {
+
+struct Geom {
+  uint64_t nwork;     // number of work items
+  uint64_t set_mask;  // bits forced to 1 (controls with value 1), in unit index space
+  int nseg;           // holes + 1
+  int pad_;
+  uint64_t seg[DSV_MAX_GEOM_SEGS];  // seg[i]: output bits that take (w << i)
+};
+
+// pdep-style expansion: bits of w between holes i-1 and i are shifted left by i.
+__device__ __forceinline__ uint64_t expand(const Geom& g, uint64_t w) {
+  uint64_t r = g.set_mask;
+  for (int i = 0; i < g.nseg; ++i) r |= (w << i) & g.seg[i];
+  return r;
+}
+
+// ---- vector "unit" traits ---------------------------------------------------
+// A unit is what one 8/16-byte access moves.  For complex64 with index bit 0
+// free, a unit is a float4 holding TWO amplitudes (index bit 0 = lane), so a
+// thread processes two groups at once with 128-bit accesses.  Otherwise a
+// unit is one amplitude (float2 for c64, double2 for c128 — 16 B).
+struct C64x2 {
+  using V = float4;
+  using R = float;
+  static constexpr int L = 2;
+  __device__ static __forceinline__ void get(const V& v, int l, R& re, R& im) {
+    if (l == 0) { re = v.x; im = v.y; } else { re = v.z; im = v.w; }
+  }
+  __device__ static __forceinline__ void set(V& v, int l, R re, R im) {
+    if (l == 0) { v.x = re; v.y = im; } else { v.z = re; v.w = im; }
+  }
+};
+struct C64x1 {
+  using V = float2;
+  using R = float;
+  static constexpr int L = 1;
+  __device__ static __forceinline__ void get(const V& v, int, R& re, R& im) { re = v.x; im = v.y; }
+  __device__ static __forceinline__ void set(V& v, int, R re, R im) { v.x = re; v.y = im; }
+};
+struct C128x1 {
+  using V = double2;
+  using R = double;
+  static constexpr int L = 1;
+  __device__ static __forceinline__ void get(const V& v, int, R& re, R& im) { re = v.x; im = v.y; }
+  __device__ static __forceinline__ void set(V& v, int, R re, R im) { v.x = re; v.y = im; }
+};
+
+template <typename R> struct cplx { R x, y; };
+
+// Exact-rounding helpers: explicit intrinsics so ptxas cannot contract or
+// reassociate (the reference multiply is NumPy's FMA form).
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// NumPy complex multiply d*a:  re = fma(dr, ar, -(di*ai)), im = fma(dr, ai, di*ar)
+template <typename R>
+__device__ __forceinline__ void cmul_numpy(R dr, R di, R ar, R ai, R& outr, R& outi) {
+  outr = fma_rn(dr, ar, -mul_rn(di, ai));
+  outi = fma_rn(dr, ai, mul_rn(di, ar));
+}
+
+// Streaming 128/64-bit global accesses.  The state is far larger than L2 and
+// every amplitude is touched once per pass.
+template <typename V> __device__ __forceinline__ V ldg_s(const V* p) { return __ldcs(p); }
+template <typename V> __device__ __forceinline__ void stg_s(V* p, const V& v) { __stcs(p, v); }
+
+// ---- block reductions (fixed order => run-to-run deterministic) ------------
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < NT / 32 ? sh[lane] : 0.0;
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+}  // namespace dsv

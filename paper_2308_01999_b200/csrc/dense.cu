@@ -1,0 +1,248 @@
+// dense.cu — dense k-qubit gate application (replaces apply_dense_bits,
+// reference statevec.py:44-60) and the fused dense expectation value
+// (replaces StateVector.expectation's copy+apply+vdot, statevec.py:241-245).
+//
+// Register path (k <= 5): each thread owns ITEMS amplitude groups (two per
+// unit in C64x2 mode), issues all 2^k loads of every group first (memory-
+// level parallelism), then streams the 2^k outputs out row by row.  The
+// 2^k x 2^k matrix lives in the kernel parameter block, i.e. the constant
+// bank: every FFMA takes its matrix operand straight from c[0x0][...], warp-
+// uniform, no shared memory.  Traffic is exactly one read + one write of the
+// control-satisfied amplitudes, the algorithmic minimum 2*s*2^(n-c).
+#include "common.cuh"
+#include "launch.h"
+
+namespace dsv {
+
+template <int K, typename R>
+struct DenseP {
+  Geom g;
+  uint64_t offs[1 << K];
+  cplx<R> m[(1 << K) * (1 << K)];
+};
+
+template <class VT, int K>
+struct DenseItems {
+  // aim for >= 64 B of loads in flight per thread
+  static constexpr int bytes = int(sizeof(typename VT::V)) << K;
+  static constexpr int value = bytes >= 64 ? 1 : 64 / bytes;
+};
+
+template <int K, class VT, int ITEMS>
+__global__ void __launch_bounds__(256)
+k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __restrict__ sv) {
+  using V = typename VT::V;
+  using R = typename VT::R;
+  constexpr int D = 1 << K;
+  constexpr int L = VT::L;
+  const uint64_t w0 = uint64_t(blockIdx.x) * (uint64_t(blockDim.x) * ITEMS) + threadIdx.x;
+  V in[ITEMS][D];
+  uint64_t base[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * blockDim.x;
+    base[it] = expand(p.g, w);
+    if (w < p.g.nwork) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) in[it][j] = ldg_s(sv + base[it] + p.offs[j]);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * blockDim.x;
+    if (w >= p.g.nwork) continue;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      R accr[L], acci[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) { accr[l] = R(0); acci[l] = R(0); }
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const R mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          R ar, ai;
+          VT::get(in[it][c], l, ar, ai);
+          accr[l] = fma(mr, ar, accr[l]);
+          accr[l] = fma(-mi, ai, accr[l]);
+          acci[l] = fma(mr, ai, acci[l]);
+          acci[l] = fma(mi, ar, acci[l]);
+        }
+      }
+      V out;
+#pragma unroll
+      for (int l = 0; l < L; ++l) VT::set(out, l, accr[l], acci[l]);
+      stg_s(sv + base[it] + p.offs[r], out);
+    }
+  }
+}
+
+template <int K, class VT>
+static cudaError_t dense_reg_t(const Geom& g, const uint64_t* offs, const void* matrix, void* sv,
+                               cudaStream_t st) {
+  using R = typename VT::R;
+  constexpr int D = 1 << K;
+  constexpr int ITEMS = DenseItems<VT, K>::value;
+  DenseP<K, R> p;
+  p.g = g;
+  for (int j = 0; j < D; ++j) p.offs[j] = offs[j];
+  const cplx<R>* m = static_cast<const cplx<R>*>(matrix);
+  for (int i = 0; i < D * D; ++i) p.m[i] = m[i];
+  const uint64_t per_block = 256ull * ITEMS;
+  const uint64_t blocks = (g.nwork + per_block - 1) / per_block;
+  if (blocks == 0) return cudaSuccess;
+  k_dense<K, VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  return cudaGetLastError();
+}
+
+template <class VT>
+static cudaError_t dense_reg_mode(int k, const Geom& g, const uint64_t* offs, const void* m,
+                                  void* sv, cudaStream_t st) {
+  switch (k) {
+    case 0: return dense_reg_t<0, VT>(g, offs, m, sv, st);
+    case 1: return dense_reg_t<1, VT>(g, offs, m, sv, st);
+    case 2: return dense_reg_t<2, VT>(g, offs, m, sv, st);
+    case 3: return dense_reg_t<3, VT>(g, offs, m, sv, st);
+    case 4: return dense_reg_t<4, VT>(g, offs, m, sv, st);
+    case 5: return dense_reg_t<5, VT>(g, offs, m, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_dense_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs,
+                             const void* matrix, void* sv, cudaStream_t st) {
+  if (dtype == 1) return dense_reg_mode<C128x1>(k, g, offs, matrix, sv, st);
+  if (mode == MODE_VEC2) return dense_reg_mode<C64x2>(k, g, offs, matrix, sv, st);
+  return dense_reg_mode<C64x1>(k, g, offs, matrix, sv, st);
+}
+
+// ---- generic path: any k <= 10 ----------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_dense_generic(const __grid_constant__ Geom g, int k, const uint64_t* __restrict__ offs,
+                const cplx<R>* __restrict__ mt, cplx<R>* __restrict__ sv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx<R>* sh = reinterpret_cast<cplx<R>*>(smem_raw);
+  const int D = 1 << k;
+  for (uint64_t w = blockIdx.x; w < g.nwork; w += gridDim.x) {
+    const uint64_t base = expand(g, w);
+    for (int j = threadIdx.x; j < D; j += blockDim.x) sh[j] = sv[base + offs[j]];
+    __syncthreads();
+    for (int r = threadIdx.x; r < D; r += blockDim.x) {
+      R ar = 0, ai = 0;
+      for (int c = 0; c < D; ++c) {
+        const cplx<R> m = mt[uint64_t(c) * D + r];
+        const cplx<R> x = sh[c];
+        ar = fma(m.x, x.x, ar);
+        ar = fma(-m.y, x.y, ar);
+        ai = fma(m.x, x.y, ai);
+        ai = fma(m.y, x.x, ai);
+      }
+      sv[base + offs[r]] = cplx<R>{ar, ai};
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_dense_generic(int dtype, int k, const Geom& g, const uint64_t* d_offs,
+                                 const void* d_matrix_t, void* sv, cudaStream_t st) {
+  if (g.nwork == 0) return cudaSuccess;
+  const unsigned blocks = unsigned(g.nwork < 148ull * 16 ? g.nwork : 148ull * 16);
+  if (dtype == 1) {
+    k_dense_generic<double><<<blocks, 256, (16u << k), st>>>(
+        g, k, d_offs, static_cast<const cplx<double>*>(d_matrix_t), static_cast<cplx<double>*>(sv));
+  } else {
+    k_dense_generic<float><<<blocks, 256, (8u << k), st>>>(
+        g, k, d_offs, static_cast<const cplx<float>*>(d_matrix_t), static_cast<cplx<float>*>(sv));
+  }
+  return cudaGetLastError();
+}
+
+// ---- fused expectation: sum_g psi_g^dagger M psi_g (read-only) ----------------
+template <int K, class VT>
+__global__ void __launch_bounds__(256)
+k_expect_dense(const __grid_constant__ DenseP<K, typename VT::R> p,
+               const typename VT::V* __restrict__ sv, double* __restrict__ partial) {
+  using V = typename VT::V;
+  using R = typename VT::R;
+  constexpr int D = 1 << K;
+  __shared__ double sh[8];
+  double er = 0.0, ei = 0.0;
+  for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < p.g.nwork;
+       w += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t base = expand(p.g, w);
+    V in[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) in[j] = ldg_s(sv + base + p.offs[j]);
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double accr = 0.0, acci = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        R ar, ai;
+        VT::get(in[c], 0, ar, ai);
+        const double mr = double(p.m[r * D + c].x), mi = double(p.m[r * D + c].y);
+        accr = fma(mr, double(ar), accr);
+        accr = fma(-mi, double(ai), accr);
+        acci = fma(mr, double(ai), acci);
+        acci = fma(mi, double(ar), acci);
+      }
+      R xr, xi;
+      VT::get(in[r], 0, xr, xi);
+      // conj(x) * acc
+      er = fma(double(xr), accr, er);
+      er = fma(double(xi), acci, er);
+      ei = fma(double(xr), acci, ei);
+      ei = fma(-double(xi), accr, ei);
+    }
+  }
+  const double sr = block_sum<256>(er, sh);
+  const double si = block_sum<256>(ei, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = sr;
+    partial[2 * blockIdx.x + 1] = si;
+  }
+}
+
+template <int K, class VT>
+static cudaError_t expect_dense_t(const Geom& g, const uint64_t* offs, const void* matrix,
+                                  const void* sv, double* d_partial, uint64_t* nchunks,
+                                  cudaStream_t st) {
+  using R = typename VT::R;
+  constexpr int D = 1 << K;
+  DenseP<K, R> p;
+  p.g = g;
+  for (int j = 0; j < D; ++j) p.offs[j] = offs[j];
+  const cplx<R>* m = static_cast<const cplx<R>*>(matrix);
+  for (int i = 0; i < D * D; ++i) p.m[i] = m[i];
+  uint64_t blocks = (g.nwork + 255) / 256;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  if (blocks == 0) blocks = 1;
+  *nchunks = blocks;
+  k_expect_dense<K, VT><<<unsigned(blocks), 256, 0, st>>>(
+      p, static_cast<const typename VT::V*>(sv), d_partial);
+  return cudaGetLastError();
+}
+
+template <class VT>
+static cudaError_t expect_dense_mode(int k, const Geom& g, const uint64_t* offs, const void* m,
+                                     const void* sv, double* d_partial, uint64_t* nchunks,
+                                     cudaStream_t st) {
+  switch (k) {
+    case 0: return expect_dense_t<0, VT>(g, offs, m, sv, d_partial, nchunks, st);
+    case 1: return expect_dense_t<1, VT>(g, offs, m, sv, d_partial, nchunks, st);
+    case 2: return expect_dense_t<2, VT>(g, offs, m, sv, d_partial, nchunks, st);
+    case 3: return expect_dense_t<3, VT>(g, offs, m, sv, d_partial, nchunks, st);
+    case 4: return expect_dense_t<4, VT>(g, offs, m, sv, d_partial, nchunks, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_expect_dense(int dtype, int k, const Geom& g, const uint64_t* offs,
+                                const void* matrix, const void* sv, double* d_partial,
+                                uint64_t* nchunks_out, cudaStream_t st) {
+  if (dtype == 1) return expect_dense_mode<C128x1>(k, g, offs, matrix, sv, d_partial, nchunks_out, st);
+  return expect_dense_mode<C64x1>(k, g, offs, matrix, sv, d_partial, nchunks_out, st);
+}
+
+}  // namespace dsv

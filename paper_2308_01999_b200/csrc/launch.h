@@ -1,0 +1,95 @@
+// launch.h — host-side launchers exported by the kernel translation units and
+// consumed by api.cu (the C ABI).  All pointers named d_* are device memory;
+// all others are host memory read during the call (kernel parameters).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace dsv {
+
+enum Mode { MODE_SCALAR = 0, MODE_VEC2 = 1 };  // VEC2: complex64 with index bit 0 free
+
+// dense k-qubit gate, k <= 5, matrix (canonical sorted-target order, state real
+// type, row-major) passed by value in the kernel parameter block
+constexpr int kDenseRegMaxK = 5;
+cudaError_t launch_dense_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs,
+                             const void* matrix, void* sv, cudaStream_t st);
+// any k <= 10: one CTA per group through shared memory, matrix transposed in HBM
+cudaError_t launch_dense_generic(int dtype, int k, const Geom& g, const uint64_t* d_offs,
+                                 const void* d_matrix_t, void* sv, cudaStream_t st);
+
+// generalised permutation, k <= 5 register path (group formation)
+constexpr int kPermRegMaxK = 5;
+// diagonal (identity permutation), any k <= 10: elementwise streaming;
+// tb = unit-space target bits (sorted), active[j] = entry j differs from 1
+cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb, const void* diag,
+                        const unsigned char* active, void* sv, cudaStream_t st);
+cudaError_t launch_perm_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs_in,
+                            const uint64_t* offs_out, const void* diag, uint64_t active,
+                            void* sv, cudaStream_t st);
+cudaError_t launch_perm_generic(int dtype, int k, const Geom& g, const uint64_t* d_offs_in,
+                                const uint64_t* d_offs_out, const void* d_diag, void* sv,
+                                cudaStream_t st);
+
+// ---- layout ---------------------------------------------------------------
+struct SwapPairs {
+  int np;
+  int a[20], b[20];  // in unit index space
+};
+cudaError_t launch_swap_bits(int dtype, int mode, uint64_t nunits, const SwapPairs& sp, void* sv,
+                             cudaStream_t st);
+cudaError_t launch_gather(int dtype, int nbits, const int32_t* ordering, uint64_t begin,
+                          uint64_t count, const void* sv, void* d_out, cudaStream_t st);
+cudaError_t launch_scatter(int dtype, int nbits, const int32_t* ordering, uint64_t begin,
+                           uint64_t count, void* sv, const void* d_in, cudaStream_t st);
+// a[off | 1<<l] <-> b[off] for off in the [lo,hi) slice of offsets with bit l clear
+cudaError_t launch_exchange_halves(int dtype, int mode, int l_unit, uint64_t lo, uint64_t hi,
+                                   void* a, void* b, cudaStream_t st);
+cudaError_t launch_exchange_all(int dtype, uint64_t namps, void* a, void* b, cudaStream_t st);
+
+// ---- elementwise ----------------------------------------------------------
+// a *= scale where (idx & mask) == val, else 0 (mask==0: plain scale)
+cudaError_t launch_collapse(int dtype, int mode, uint64_t nunits, uint64_t mask, uint64_t val,
+                            double scale, void* sv, cudaStream_t st);
+struct PauliOp {
+  uint64_t xmask;   // X|Y bits
+  uint64_t yzmask;  // Y|Z bits (sign bits)
+  int hbit;         // highest bit of xmask (-1 if none)
+  double c;         // coefficient on psi_i (cos(theta/2), or 0 for a pure product)
+  double br, bi;    // complex factor on (-1)^popcount(i & yzmask) psi_{i^x}
+};
+cudaError_t launch_pauli(int dtype, int nbits, const PauliOp& op, void* sv, cudaStream_t st);
+
+// ---- reductions -------------------------------------------------------------
+// probability bins: partial[bin*nchunks + chunk]; bins over `bits` (bit j of bin -> bits[j])
+constexpr int kReduceThreads = 256;
+constexpr int kReduceUnitsPerThread = 16;
+struct BinGeom {
+  Geom g;            // free-bit expansion (holes = binned bits), in unit space
+  int nb;            // number of binned bits
+  int bits[40];      // unit-space bit of bin bit j
+  uint64_t nchunks;  // chunks per bin
+};
+cudaError_t launch_probs(int dtype, int mode, const BinGeom& bg, const void* sv, double* d_partial,
+                         cudaStream_t st);
+// final reduction: out[b*ncomp + c] = sum_k partial[(b*nchunks + k)*ncomp + c]
+cudaError_t launch_final_sum(uint64_t nbins, uint64_t nchunks, int ncomp, const double* d_partial,
+                             double* d_out, cudaStream_t st);
+// <psi|P|psi>: 2 components per chunk
+cudaError_t launch_expect_pauli(int dtype, int nbits, const PauliOp& op, const void* sv,
+                                double* d_partial, uint64_t* nchunks_out, cudaStream_t st);
+cudaError_t launch_inner(int dtype, uint64_t namps, const void* a, const void* b,
+                         double* d_partial, uint64_t* nchunks_out, cudaStream_t st);
+cudaError_t launch_expect_dense(int dtype, int k, const Geom& g, const uint64_t* offs,
+                                const void* matrix, const void* sv, double* d_partial,
+                                uint64_t* nchunks_out, cudaStream_t st);
+// sampling: per shot, scan chunk[s] (CH amps) for the first index where the
+// running |a|^2 exceeds resid[s]
+cudaError_t launch_sample_scan(int dtype, uint64_t namps, uint64_t chunk_amps, int64_t shots,
+                               const uint64_t* d_chunk, const double* d_resid, const void* sv,
+                               uint64_t* d_out, cudaStream_t st);
+
+uint64_t chunks_for(uint64_t nunits);
+
+}  // namespace dsv

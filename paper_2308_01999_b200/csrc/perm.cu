@@ -1,0 +1,250 @@
+// perm.cu — generalised-permutation / diagonal gate application (replaces
+// apply_permutation_bits, reference statevec.py:63-81):
+//     out[perm[j]] = diag[j] * in[j]     for every control-satisfied group.
+//
+// Bit-exact with the reference: the product is NumPy's FMA form
+// (re = fma(dr, ar, -(di*ai)), im = fma(dr, ai, di*ar)), written with
+// explicit round-to-nearest intrinsics so ptxas cannot re-contract it.
+//
+// Table entries with perm[j] == j and diag[j] == 1 are skipped entirely (the
+// `active` mask): their amplitudes are neither read nor written.  The active
+// set is closed under perm, so reading only active inputs and writing only
+// active outputs is complete.  For an unfused controlled phase this halves
+// the touched amplitudes on top of the control subcube (2*s*2^(n-2) bytes).
+#include "common.cuh"
+#include "launch.h"
+
+#define DSV_MAX_TARGETS_ 10
+
+namespace dsv {
+
+template <int K, typename R>
+struct PermP {
+  Geom g;
+  uint64_t active;  // bit j set: entry j moves or scales
+  uint64_t offs_in[1 << K];
+  uint64_t offs_out[1 << K];  // offs[perm[j]]
+  cplx<R> d[1 << K];
+};
+
+template <class VT, int K>
+struct PermItems {
+  static constexpr int bytes = int(sizeof(typename VT::V)) << K;
+  static constexpr int value = bytes >= 64 ? 1 : 64 / bytes;
+};
+
+template <int K, class VT, int ITEMS>
+__global__ void __launch_bounds__(256)
+k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __restrict__ sv) {
+  using V = typename VT::V;
+  using R = typename VT::R;
+  constexpr int D = 1 << K;
+  constexpr int L = VT::L;
+  const uint64_t w0 = uint64_t(blockIdx.x) * (uint64_t(blockDim.x) * ITEMS) + threadIdx.x;
+  V in[ITEMS][D];
+  uint64_t base[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * blockDim.x;
+    base[it] = expand(p.g, w);
+    if (w < p.g.nwork) {
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        if ((p.active >> j) & 1ull) in[it][j] = ldg_s(sv + base[it] + p.offs_in[j]);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * blockDim.x;
+    if (w >= p.g.nwork) continue;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if (!((p.active >> j) & 1ull)) continue;
+      const R dr = p.d[j].x, di = p.d[j].y;
+      V out;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        R ar, ai, orr, oi;
+        VT::get(in[it][j], l, ar, ai);
+        cmul_numpy(dr, di, ar, ai, orr, oi);
+        VT::set(out, l, orr, oi);
+      }
+      stg_s(sv + base[it] + p.offs_out[j], out);
+    }
+  }
+}
+
+template <int K, class VT>
+static cudaError_t perm_reg_t(const Geom& g, const uint64_t* offs_in, const uint64_t* offs_out,
+                              const void* diag, uint64_t active, void* sv, cudaStream_t st) {
+  using R = typename VT::R;
+  constexpr int D = 1 << K;
+  constexpr int ITEMS = PermItems<VT, K>::value;
+  PermP<K, R> p;
+  p.g = g;
+  p.active = active;
+  const cplx<R>* d = static_cast<const cplx<R>*>(diag);
+  for (int j = 0; j < D; ++j) {
+    p.offs_in[j] = offs_in[j];
+    p.offs_out[j] = offs_out[j];
+    p.d[j] = d[j];
+  }
+  const uint64_t per_block = 256ull * ITEMS;
+  const uint64_t blocks = (g.nwork + per_block - 1) / per_block;
+  if (blocks == 0 || active == 0) return cudaSuccess;
+  k_perm<K, VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  return cudaGetLastError();
+}
+
+template <class VT>
+static cudaError_t perm_reg_mode(int k, const Geom& g, const uint64_t* oi, const uint64_t* oo,
+                                 const void* d, uint64_t a, void* sv, cudaStream_t st) {
+  switch (k) {
+    case 0: return perm_reg_t<0, VT>(g, oi, oo, d, a, sv, st);
+    case 1: return perm_reg_t<1, VT>(g, oi, oo, d, a, sv, st);
+    case 2: return perm_reg_t<2, VT>(g, oi, oo, d, a, sv, st);
+    case 3: return perm_reg_t<3, VT>(g, oi, oo, d, a, sv, st);
+    case 4: return perm_reg_t<4, VT>(g, oi, oo, d, a, sv, st);
+    case 5: return perm_reg_t<5, VT>(g, oi, oo, d, a, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_perm_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs_in,
+                            const uint64_t* offs_out, const void* diag, uint64_t active, void* sv,
+                            cudaStream_t st) {
+  if (dtype == 1) return perm_reg_mode<C128x1>(k, g, offs_in, offs_out, diag, active, sv, st);
+  if (mode == MODE_VEC2) return perm_reg_mode<C64x2>(k, g, offs_in, offs_out, diag, active, sv, st);
+  return perm_reg_mode<C64x1>(k, g, offs_in, offs_out, diag, active, sv, st);
+}
+
+
+// ---- diagonal gates: elementwise streaming, any k <= 10 ---------------------------
+// A diagonal needs no group formation: each amplitude is scaled by
+// diag[j(idx)] where j gathers the target bits of its own index.  Work items
+// enumerate the control-satisfied subcube only (holes = control bits), the
+// target bits stay inside the contiguous run, so every warp access is a
+// fully coalesced 128-bit stream.  Units whose table entry is exactly 1 are
+// neither read nor written.  The table lives in shared memory (lanes index
+// it with different j when targets are low bits).
+template <typename R>
+struct DiagP {
+  Geom g;                 // holes = controls, unit space
+  int k;
+  int tb[DSV_MAX_TARGETS_];  // unit-space target bits, sorted
+  cplx<R> d[1 << DSV_MAX_TARGETS_];
+  unsigned char active[1 << DSV_MAX_TARGETS_];
+};
+
+template <class VT, int ITEMS>
+__global__ void __launch_bounds__(256)
+k_diag(const __grid_constant__ DiagP<typename VT::R> p, typename VT::V* __restrict__ sv) {
+  using V = typename VT::V;
+  using R = typename VT::R;
+  __shared__ cplx<R> sd[1 << DSV_MAX_TARGETS_];
+  __shared__ unsigned char sa[1 << DSV_MAX_TARGETS_];
+  const int D = 1 << p.k;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    sd[j] = p.d[j];
+    sa[j] = p.active[j];
+  }
+  __syncthreads();
+  const uint64_t w0 = uint64_t(blockIdx.x) * (uint64_t(blockDim.x) * ITEMS) + threadIdx.x;
+  V v[ITEMS];
+  uint64_t idx[ITEMS];
+  int jj[ITEMS];
+  bool on[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * blockDim.x;
+    idx[it] = expand(p.g, w);
+    int j = 0;
+    for (int m = 0; m < p.k; ++m) j |= int((idx[it] >> p.tb[m]) & 1ull) << m;
+    jj[it] = j;
+    on[it] = (w < p.g.nwork) && sa[j];
+    if (on[it]) v[it] = ldg_s(sv + idx[it]);
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    if (!on[it]) continue;
+    const cplx<R> d = sd[jj[it]];
+#pragma unroll
+    for (int l = 0; l < VT::L; ++l) {
+      R ar, ai, orr, oi;
+      VT::get(v[it], l, ar, ai);
+      cmul_numpy(d.x, d.y, ar, ai, orr, oi);
+      VT::set(v[it], l, orr, oi);
+    }
+    stg_s(sv + idx[it], v[it]);
+  }
+}
+
+template <class VT>
+static cudaError_t diag_t(const Geom& g, int k, const int* tb, const void* diag,
+                          const unsigned char* active, void* sv, cudaStream_t st) {
+  using R = typename VT::R;
+  constexpr int ITEMS = sizeof(typename VT::V) == 16 ? 4 : 8;
+  DiagP<R> p;
+  p.g = g;
+  p.k = k;
+  for (int m = 0; m < DSV_MAX_TARGETS_; ++m) p.tb[m] = m < k ? tb[m] : 0;
+  const cplx<R>* d = static_cast<const cplx<R>*>(diag);
+  for (int j = 0; j < (1 << k); ++j) {
+    p.d[j] = d[j];
+    p.active[j] = active[j];
+  }
+  const uint64_t per_block = 256ull * ITEMS;
+  const uint64_t blocks = (g.nwork + per_block - 1) / per_block;
+  if (blocks == 0) return cudaSuccess;
+  k_diag<VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb, const void* diag,
+                        const unsigned char* active, void* sv, cudaStream_t st) {
+  if (dtype == 1) return diag_t<C128x1>(g, k, tb, diag, active, sv, st);
+  if (mode == MODE_VEC2) return diag_t<C64x2>(g, k, tb, diag, active, sv, st);
+  return diag_t<C64x1>(g, k, tb, diag, active, sv, st);
+}
+
+// ---- generic path: k <= 10, one CTA per group through shared memory -----------
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_perm_generic(const __grid_constant__ Geom g, int k, const uint64_t* __restrict__ offs_in,
+               const uint64_t* __restrict__ offs_out, const cplx<R>* __restrict__ diag,
+               cplx<R>* __restrict__ sv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx<R>* sh = reinterpret_cast<cplx<R>*>(smem_raw);
+  const int D = 1 << k;
+  for (uint64_t w = blockIdx.x; w < g.nwork; w += gridDim.x) {
+    const uint64_t base = expand(g, w);
+    for (int j = threadIdx.x; j < D; j += blockDim.x) sh[j] = sv[base + offs_in[j]];
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      const cplx<R> d = diag[j], a = sh[j];
+      cplx<R> o;
+      cmul_numpy(d.x, d.y, a.x, a.y, o.x, o.y);
+      sv[base + offs_out[j]] = o;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_perm_generic(int dtype, int k, const Geom& g, const uint64_t* d_offs_in,
+                                const uint64_t* d_offs_out, const void* d_diag, void* sv,
+                                cudaStream_t st) {
+  if (g.nwork == 0) return cudaSuccess;
+  const unsigned blocks = unsigned(g.nwork < 148ull * 16 ? g.nwork : 148ull * 16);
+  if (dtype == 1) {
+    k_perm_generic<double><<<blocks, 256, (16u << k), st>>>(
+        g, k, d_offs_in, d_offs_out, static_cast<const cplx<double>*>(d_diag),
+        static_cast<cplx<double>*>(sv));
+  } else {
+    k_perm_generic<float><<<blocks, 256, (8u << k), st>>>(
+        g, k, d_offs_in, d_offs_out, static_cast<const cplx<float>*>(d_diag),
+        static_cast<cplx<float>*>(sv));
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dsv

@@ -1,0 +1,249 @@
+// reduce.cu — read-only reductions over the state (float64 accumulation,
+// fixed summation order => bit-reproducible run to run):
+//   * marginal probabilities / norm  (marginal_probabilities_bits, statevec.py:107-113;
+//                                     norm_squared, core.py:62-71)
+//   * Pauli-string expectation       (StateVector.expectation, statevec.py:246-253,
+//                                     without the full-size copy)
+//   * <a|b>                          (np.vdot)
+//   * sampling scan                  (StateVector.sample, statevec.py:267-272)
+//
+// Each kernel writes one partial per (bin, chunk) block; launch_final_sum
+// folds the partials of a bin in chunk order.  Block order is chunk-major
+// with all bins of a chunk adjacent, so when the binned bits are low index
+// bits the 2^k blocks sharing the same 128-B lines run concurrently and the
+// lines are fetched from HBM once (L2 hit for the sibling bins).
+#include "common.cuh"
+#include "launch.h"
+
+namespace dsv {
+
+constexpr uint64_t kChunkUnits = uint64_t(kReduceThreads) * kReduceUnitsPerThread;
+
+uint64_t chunks_for(uint64_t nunits) {
+  uint64_t c = (nunits + kChunkUnits - 1) / kChunkUnits;
+  return c ? c : 1;
+}
+
+template <class VT>
+__global__ void __launch_bounds__(kReduceThreads)
+k_probs(const typename VT::V* __restrict__ sv, const __grid_constant__ BinGeom bg,
+        double* __restrict__ partial) {
+  using V = typename VT::V;
+  using R = typename VT::R;
+  __shared__ double sh[kReduceThreads / 32];
+  const uint64_t nbins = 1ull << bg.nb;
+  const uint64_t chunk = blockIdx.x / nbins;
+  const uint64_t bin = blockIdx.x % nbins;
+  uint64_t bin_base = 0;
+  for (int j = 0; j < bg.nb; ++j) bin_base |= ((bin >> j) & 1ull) << bg.bits[j];
+  double acc = 0.0;
+  const uint64_t f0 = chunk * kChunkUnits + threadIdx.x;
+  constexpr int kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    V v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t f = f0 + uint64_t(u0 + u) * kReduceThreads;
+      if (f < bg.g.nwork) v[u] = ldg_s(sv + (expand(bg.g, f) | bin_base));
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t f = f0 + uint64_t(u0 + u) * kReduceThreads;
+      if (f < bg.g.nwork) {
+#pragma unroll
+        for (int l = 0; l < VT::L; ++l) {
+          R re, im;
+          VT::get(v[u], l, re, im);
+          acc = fma(double(re), double(re), acc);
+          acc = fma(double(im), double(im), acc);
+        }
+      }
+    }
+  }
+  const double s = block_sum<kReduceThreads>(acc, sh);
+  if (threadIdx.x == 0) partial[bin * bg.nchunks + chunk] = s;
+}
+
+cudaError_t launch_probs(int dtype, int mode, const BinGeom& bg, const void* sv, double* d_partial,
+                         cudaStream_t st) {
+  const uint64_t blocks = bg.nchunks << bg.nb;
+  if (dtype == 1)
+    k_probs<C128x1><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const double2*>(sv), bg, d_partial);
+  else if (mode == MODE_VEC2)
+    k_probs<C64x2><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float4*>(sv), bg, d_partial);
+  else
+    k_probs<C64x1><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float2*>(sv), bg, d_partial);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256)
+k_final_sum(uint64_t nchunks, int ncomp, const double* __restrict__ partial, double* __restrict__ out) {
+  __shared__ double sh[8];
+  const uint64_t bin = blockIdx.x;
+  for (int c = 0; c < ncomp; ++c) {
+    double acc = 0.0;
+    for (uint64_t k = threadIdx.x; k < nchunks; k += blockDim.x)
+      acc += partial[(bin * nchunks + k) * ncomp + c];
+    const double s = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) out[bin * ncomp + c] = s;
+  }
+}
+
+cudaError_t launch_final_sum(uint64_t nbins, uint64_t nchunks, int ncomp, const double* d_partial,
+                             double* d_out, cudaStream_t st) {
+  k_final_sum<<<unsigned(nbins), 256, 0, st>>>(nchunks, ncomp, d_partial, d_out);
+  return cudaGetLastError();
+}
+
+// ---- Pauli expectation ----------------------------------------------------------------
+// <psi|P|psi> = sum_i conj(psi_i) (P psi)_i with (P psi)_i = B s(i) psi_{i^x},
+// B = (-i)^{#Y}, s(i) = (-1)^popcount(i & yz).  Each pair (i, i^x) is read
+// once and contributes both of its terms.
+template <typename V, typename R>
+__global__ void __launch_bounds__(kReduceThreads)
+k_expect_pauli(const V* __restrict__ sv, uint64_t npairs, const __grid_constant__ PauliOp op,
+               double* __restrict__ partial) {
+  __shared__ double sh[kReduceThreads / 32];
+  const int h = op.hbit;
+  const uint64_t lowmask = h >= 0 ? (1ull << h) - 1ull : 0ull;
+  double er = 0.0, ei = 0.0;
+  const uint64_t t0 = uint64_t(blockIdx.x) * kChunkUnits + threadIdx.x;
+#pragma unroll 4
+  for (int u = 0; u < kReduceUnitsPerThread; ++u) {
+    const uint64_t t = t0 + uint64_t(u) * kReduceThreads;
+    if (t >= npairs) break;
+    if (h < 0) {
+      const V a = ldg_s(sv + t);
+      const double sg = (__popcll(t & op.yzmask) & 1) ? -1.0 : 1.0;
+      const double p = double(a.x) * double(a.x) + double(a.y) * double(a.y);
+      er = fma(sg, p, er);
+    } else {
+      const uint64_t i = ((t & ~lowmask) << 1) | (t & lowmask);
+      const uint64_t j = i ^ op.xmask;
+      const V a = ldg_s(sv + i);
+      const V b = ldg_s(sv + j);
+      const double ar = a.x, ai = a.y, br = b.x, bi = b.y;
+      const double si = (__popcll(i & op.yzmask) & 1) ? -1.0 : 1.0;
+      const double sj = (__popcll(j & op.yzmask) & 1) ? -1.0 : 1.0;
+      // q = B * b ; term_i = conj(a) * q * si
+      const double qr = op.br * br - op.bi * bi, qi = op.br * bi + op.bi * br;
+      er += si * (ar * qr + ai * qi);
+      ei += si * (ar * qi - ai * qr);
+      // q' = B * a ; term_j = conj(b) * q' * sj
+      const double pr = op.br * ar - op.bi * ai, pi = op.br * ai + op.bi * ar;
+      er += sj * (br * pr + bi * pi);
+      ei += sj * (br * pi - bi * pr);
+    }
+  }
+  const double sr = block_sum<kReduceThreads>(er, sh);
+  const double si = block_sum<kReduceThreads>(ei, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = sr;
+    partial[2 * blockIdx.x + 1] = si;
+  }
+}
+
+cudaError_t launch_expect_pauli(int dtype, int nbits, const PauliOp& op, const void* sv,
+                                double* d_partial, uint64_t* nchunks_out, cudaStream_t st) {
+  const uint64_t n = 1ull << nbits;
+  const uint64_t npairs = op.hbit >= 0 ? n / 2 : n;
+  const uint64_t blocks = chunks_for(npairs);
+  *nchunks_out = blocks;
+  if (dtype == 1)
+    k_expect_pauli<double2, double><<<unsigned(blocks), kReduceThreads, 0, st>>>(
+        static_cast<const double2*>(sv), npairs, op, d_partial);
+  else
+    k_expect_pauli<float2, float><<<unsigned(blocks), kReduceThreads, 0, st>>>(
+        static_cast<const float2*>(sv), npairs, op, d_partial);
+  return cudaGetLastError();
+}
+
+// ---- <a|b> ----------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(kReduceThreads)
+k_inner(const V* __restrict__ a, const V* __restrict__ b, uint64_t n, double* __restrict__ partial) {
+  __shared__ double sh[kReduceThreads / 32];
+  double er = 0.0, ei = 0.0;
+  const uint64_t t0 = uint64_t(blockIdx.x) * kChunkUnits + threadIdx.x;
+#pragma unroll 4
+  for (int u = 0; u < kReduceUnitsPerThread; ++u) {
+    const uint64_t t = t0 + uint64_t(u) * kReduceThreads;
+    if (t >= n) break;
+    const V x = ldg_s(a + t), y = ldg_s(b + t);
+    er += double(x.x) * double(y.x) + double(x.y) * double(y.y);
+    ei += double(x.x) * double(y.y) - double(x.y) * double(y.x);
+  }
+  const double sr = block_sum<kReduceThreads>(er, sh);
+  const double si = block_sum<kReduceThreads>(ei, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = sr;
+    partial[2 * blockIdx.x + 1] = si;
+  }
+}
+
+cudaError_t launch_inner(int dtype, uint64_t namps, const void* a, const void* b,
+                         double* d_partial, uint64_t* nchunks_out, cudaStream_t st) {
+  const uint64_t blocks = chunks_for(namps);
+  *nchunks_out = blocks;
+  if (dtype == 1)
+    k_inner<double2><<<unsigned(blocks), kReduceThreads, 0, st>>>(
+        static_cast<const double2*>(a), static_cast<const double2*>(b), namps, d_partial);
+  else
+    k_inner<float2><<<unsigned(blocks), kReduceThreads, 0, st>>>(
+        static_cast<const float2*>(a), static_cast<const float2*>(b), namps, d_partial);
+  return cudaGetLastError();
+}
+
+// ---- sampling: warp per shot, scan one chunk with an inclusive warp prefix ----------------
+template <typename V>
+__global__ void __launch_bounds__(256)
+k_sample_scan(const V* __restrict__ sv, uint64_t namps, uint64_t chunk_amps, int64_t shots,
+              const uint64_t* __restrict__ chunk, const double* __restrict__ resid,
+              uint64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (s >= shots) return;
+  const uint64_t begin = chunk[s] * chunk_amps;
+  uint64_t end = begin + chunk_amps;
+  if (end > namps) end = namps;
+  const double target = resid[s];
+  double run = 0.0;
+  uint64_t found = end - 1;  // rounding fallback: last amplitude of the chunk
+  for (uint64_t i0 = begin; i0 < end; i0 += 32) {
+    const uint64_t i = i0 + lane;
+    double p = 0.0;
+    if (i < end) {
+      const V a = sv[i];
+      p = double(a.x) * double(a.x) + double(a.y) * double(a.y);
+    }
+    // inclusive scan across the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double q = __shfl_up_sync(0xffffffffu, p, o);
+      if (lane >= o) p += q;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, (i < end) && (run + p > target));
+    if (hit) {
+      found = i0 + __ffs(hit) - 1;
+      break;
+    }
+    run += __shfl_sync(0xffffffffu, p, 31);
+  }
+  if (lane == 0) out[s] = found;
+}
+
+cudaError_t launch_sample_scan(int dtype, uint64_t namps, uint64_t chunk_amps, int64_t shots,
+                               const uint64_t* d_chunk, const double* d_resid, const void* sv,
+                               uint64_t* d_out, cudaStream_t st) {
+  const uint64_t blocks = (uint64_t(shots) * 32 + 255) / 256;
+  if (dtype == 1)
+    k_sample_scan<double2><<<unsigned(blocks), 256, 0, st>>>(static_cast<const double2*>(sv), namps,
+                                                            chunk_amps, shots, d_chunk, d_resid, d_out);
+  else
+    k_sample_scan<float2><<<unsigned(blocks), 256, 0, st>>>(static_cast<const float2*>(sv), namps,
+                                                           chunk_amps, shots, d_chunk, d_resid, d_out);
+  return cudaGetLastError();
+}
+
+}  // namespace dsv

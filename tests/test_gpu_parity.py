@@ -1,0 +1,388 @@
+"""GPU parity: the CUDA engine against the reference's golden vectors and the
+CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): generalised permutations, diagonals and
+index-bit swaps are BIT-EXACT (IEEE equality); everything else within
+max|d| <= 1e-5 (complex64) / 1e-12 (complex128)."""
+
+import numpy as np
+import pytest
+
+from conftest import gate_from_spec, golden, random_state
+from oracle import sv_oracle as O
+from paper_2308_01999_b200 import _native as N
+from paper_2308_01999_b200 import gates as G
+from paper_2308_01999_b200.circuits import gen_qft, to_gates
+from paper_2308_01999_b200.core import InvalidArgumentError
+from paper_2308_01999_b200.distsim import SegmentedStateVector
+from paper_2308_01999_b200.fusion import FusionConfig, fuse
+from paper_2308_01999_b200.statevec import StateVector, run_circuit_sv
+
+pytestmark = pytest.mark.gpu
+
+DT = {"complex64": np.complex64, "complex128": np.complex128}
+TOL = {"complex64": 1e-5, "complex128": 1e-12, np.dtype(np.complex64): 1e-5, np.dtype(np.complex128): 1e-12}
+SQ2 = 1 / np.sqrt(2)
+
+
+@pytest.fixture(autouse=True)
+def _gpu(gpu_available):
+    return gpu_available
+
+
+def sv_from(amps):
+    return StateVector.from_amplitudes(np.asarray(amps))
+
+
+# ---- golden vectors from the reference ------------------------------------------------------
+
+def test_golden_single_ops():
+    nexact = 0
+    for case in golden("single_ops"):
+        g = gate_from_spec(case["gate"])
+        sv = sv_from(case["in"])
+        sv.apply(g)
+        got = sv.amplitudes
+        if case["gate"]["kind"] == "perm":
+            np.testing.assert_array_equal(got, case["out"])
+            nexact += 1
+        else:
+            np.testing.assert_allclose(got, case["out"], atol=TOL[case["dtype"]], rtol=0)
+    assert nexact > 100
+
+
+def test_golden_random_circuits():
+    for case in golden("sv_random"):
+        gates = [gate_from_spec(s) for s in case["gates"]]
+        sv = run_circuit_sv(gates, case["n"], dtype=DT[case["dtype"]])
+        assert sv.amplitudes.dtype == DT[case["dtype"]]
+        np.testing.assert_allclose(sv.amplitudes, case["out"], atol=TOL[case["dtype"]], rtol=0)
+
+
+def test_golden_swap_and_access():
+    for c in golden("swap_access"):
+        sv = sv_from(c["in"])
+        sv.swap_index_bits(c["pairs"])
+        np.testing.assert_array_equal(sv.amplitudes, c["out"])
+        assert sv.bit_map == c["bit_map"]
+        np.testing.assert_array_equal(sv.access(c["ordering"], c["begin"], c["end"]), c["access"])
+        np.testing.assert_array_equal(sv.logical_amplitudes(), c["logical"])
+        sv2 = sv_from(c["in"])
+        sv2.access_set(c["ordering"], c["begin"], c["set_values"])
+        np.testing.assert_array_equal(sv2.amplitudes, c["after_set"])
+
+
+def test_golden_measure_expectation_rotation_sample():
+    mism = 0
+    for c in golden("measure"):
+        n, st = c["n"], c["in"]
+        tol = TOL[c["dtype"]]
+        sv = sv_from(st)
+        p = sv.probabilities(c["qubits"])
+        assert p.dtype == c["probs"].dtype
+        np.testing.assert_allclose(p, c["probs"], atol=max(tol, 1e-6))
+        assert sv.measure(c["qubits"], c["r"]) == c["outcome"]
+        np.testing.assert_allclose(sv.amplitudes, c["collapsed"], atol=max(tol, 1e-6))
+        sv3 = sv_from(st)
+        paulis = [G.PauliString(f, coef) for f, coef in c["paulis"]]
+        assert abs(sv3.expectation(paulis) - c["ev_pauli"]) < 1e-5
+        ev = sv3.expectation(G.DenseGate(c["herm"], c["herm_targets"], unitary=False))
+        assert abs(ev - c["ev_dense"]) < 1e-5
+        np.testing.assert_array_equal(sv3.amplitudes, st)  # expectation leaves the state untouched
+        assert abs(sv3.norm_squared() - c["norm"]) < 1e-6
+        sv4 = sv_from(st)
+        sv4.apply_pauli_rotation(c["theta"], G.PauliString(*c["rot"]))
+        np.testing.assert_allclose(sv4.amplitudes, c["rotated"], atol=max(tol, 1e-6))
+        shots = sv3.sample(len(c["shots"]), qubit_order=c["order"], seed=c["seed"])
+        mism += sum(a != b for a, b in zip(shots, c["shots"]))
+    # the reference's CDF is a float32 cumsum for complex64; near-boundary
+    # variates may land on the neighbouring outcome
+    assert mism <= 2
+
+
+def test_golden_fusion_circuits_run_on_gpu():
+    for case in golden("fusion")["cases"]:
+        gates = [gate_from_spec(s) for s in case["gates"]]
+        fc = fuse(gates, FusionConfig(*case["cfg"]))
+        sv = run_circuit_sv(fc.gates, case["n"])
+        np.testing.assert_allclose(sv.amplitudes, case["out"], atol=1e-10)
+
+
+def test_golden_segmented_runs():
+    for c in golden("distsim")["runs"]:
+        gates = [gate_from_spec(s) for s in c["gates"]]
+        with SegmentedStateVector(c["n"], c["g"], c["workers"]) as ssv:
+            ssv.run(gates)
+            assert ssv.transfer_stats().as_dict() == c["stats"]
+            assert ssv.qubit_map == c["qubit_map"]
+            for got, want in zip(ssv.segments, c["segments"]):
+                # reference distsim computes c128 gate data for c128 states: same as ours
+                np.testing.assert_allclose(got, want, atol=1e-12)
+            np.testing.assert_allclose(ssv.to_statevector().amplitudes, c["logical"], atol=1e-12)
+
+
+def test_golden_segmented_swaps_bit_exact():
+    for c in golden("distsim")["swaps"]:
+        n, g = c["n"], c["g"]
+        ssv = SegmentedStateVector(n, g, c["workers"])
+        L = 1 << (n - g)
+        for s in range(1 << g):
+            ssv.segments[s][:] = c["in"][s * L:(s + 1) * L]
+        ssv.distributed_index_bit_swap(c["pairs"])
+        for got, want in zip(ssv.segments, c["segments"]):
+            np.testing.assert_array_equal(got, want)
+        assert ssv.stats.as_dict() == c["stats"]
+        assert ssv.qubit_map == c["qubit_map"]
+
+
+def test_golden_dump_bytes(tmp_path):
+    d = golden("misc")["dump"]
+    sv = sv_from(d["in"])
+    sv.swap_index_bits(d["pairs"])
+    p = tmp_path / "s.bin"
+    sv.dump(p)
+    assert p.read_bytes() == d["bytes"]
+    back = StateVector.load(p)
+    assert back.num_qubits == 5
+    np.testing.assert_array_equal(back.amplitudes, sv.logical_amplitudes())
+
+
+def test_golden_qft_states():
+    for n, want in golden("misc")["qft_states"].items():
+        np.testing.assert_allclose(run_circuit_sv(to_gates(gen_qft(n)), n).amplitudes, want, atol=1e-12)
+
+
+# ---- known answers (reference test_statevec.py / test_circuits.py) ---------------------------
+
+def test_known_answers():
+    sv = StateVector(1)
+    sv.apply_matrix(G.h(0))
+    np.testing.assert_allclose(sv.amplitudes, [SQ2, SQ2], atol=1e-15)
+    sv = sv_from(np.array([0, 0, 1, 0], dtype=complex))
+    sv.apply_matrix(G.DenseGate(G.PAULI_MATS["X"], (0,), controls=((1, 1),)))
+    np.testing.assert_allclose(sv.amplitudes, [0, 0, 0, 1], atol=1e-15)
+    sv = sv_from(np.array([0, 0, 1, 0], dtype=complex))
+    sv.apply_matrix(G.DenseGate(G.PAULI_MATS["X"], (0,), controls=((1, 0),)))
+    np.testing.assert_allclose(sv.amplitudes, [0, 0, 1, 0], atol=1e-15)
+    sv = StateVector(1)
+    sv.apply_pauli_rotation(np.pi, G.PauliString(((0, "Z"),)))
+    np.testing.assert_allclose(sv.amplitudes, [-1j, 0], atol=1e-15)
+    for rv, want in [(0.49, 0), (0.51, 1)]:
+        assert sv_from(np.array([SQ2, SQ2], dtype=complex)).measure([0], rv, collapse=False) == want
+    ghz = sv_from(np.array([SQ2, 0, 0, 0, 0, 0, 0, SQ2], dtype=complex))
+    assert abs(ghz.expectation([G.PauliString(((0, "Z"), (1, "Z")))]) - 1.0) < 1e-12
+    assert sv_from(np.array([0, 0, 0, 0, 0, 1, 0, 0], dtype=complex)).sample(100, seed=99) == ["101"] * 100
+    sv = sv_from(np.array([1, 2, 3, 4], dtype=complex))
+    sv.swap_index_bits([(0, 1)])
+    np.testing.assert_array_equal(sv.amplitudes, [1, 3, 2, 4])
+    assert sv.bit_map == [1, 0]
+    np.testing.assert_array_equal(sv_from(np.array([1, 2, 3, 4], dtype=complex)).access([1, 0]), [1, 3, 2, 4])
+
+
+def test_qft_is_dft_and_host_mirror_writes():
+    n, dim = 3, 8
+    w = np.exp(2j * np.pi / dim)
+    dft = np.array([[w ** (x * y) for x in range(dim)] for y in range(dim)]) / np.sqrt(dim)
+    gates = to_gates(gen_qft(n))
+    for x in range(dim):
+        sv = run_circuit_sv([], n)
+        amps = np.zeros(dim, dtype=complex)
+        amps[x] = 1
+        sv.amplitudes[:] = amps  # in-place write to the host mirror, re-uploaded lazily
+        for g in gates:
+            sv.apply(g)
+        np.testing.assert_allclose(sv.amplitudes, dft[:, x], atol=1e-12)
+
+
+def test_uniform_sampling_statistics_and_determinism():
+    sv = StateVector(4)
+    for q in range(4):
+        sv.apply_matrix(G.h(q))
+    shots = sv.sample(100_000, seed=7)
+    means = np.array([[int(ch) for ch in s] for s in shots]).mean(axis=0)
+    assert np.all(means >= 0.494) and np.all(means <= 0.506)
+    rs = sv_from(random_state(5, np.random.default_rng(31)))
+    assert rs.sample(500, seed=5) == rs.sample(500, seed=5)
+
+
+# ---- engine coverage vs the oracle: every kernel path --------------------------------------------
+
+def _check(got, want, dtype, exact):
+    if exact:
+        np.testing.assert_array_equal(got, want)
+    else:
+        np.testing.assert_allclose(got, want, atol=TOL[np.dtype(dtype)] * 10, rtol=0)
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("k", list(range(1, 11)))
+def test_dense_all_arities_vs_oracle(dtype, k):
+    rng = np.random.default_rng(100 + k)
+    for trial in range(4):
+        n = int(rng.integers(k, k + 5)) if k < 9 else k + trial % 2
+        n = max(n, k)
+        qs = rng.permutation(n).tolist()
+        targets = qs[:k]
+        if trial == 0 and 0 not in targets:
+            targets[0] = 0  # force index bit 0 into the targets (scalar path)
+            qs = targets + [q for q in range(n) if q not in targets]
+        ctrls = [(q, int(rng.integers(0, 2))) for q in qs[k:k + min(2, n - k)]] if trial % 2 else []
+        st = random_state(n, rng, dtype)
+        m = G.random_unitary(1 << k, rng)
+        want = st.copy()
+        O.apply_dense(want, n, m, targets, ctrls)
+        sv = sv_from(st)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
+        _check(sv.amplitudes, want, dtype, exact=False)
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("k", list(range(1, 9)))
+def test_genperm_and_diag_all_arities_bit_exact(dtype, k):
+    rng = np.random.default_rng(200 + k)
+    for trial in range(6):
+        n = int(rng.integers(k, k + 6))
+        qs = rng.permutation(n).tolist()
+        targets = qs[:k]
+        ctrls = [(q, int(rng.integers(0, 2))) for q in qs[k:k + min(2, n - k)]] if trial % 2 else []
+        st = random_state(n, rng, dtype)
+        diag = np.exp(1j * rng.uniform(0, 2 * np.pi, 1 << k))
+        diag[rng.random(1 << k) < 0.25] = 1.0
+        perm = np.arange(1 << k) if trial < 3 else rng.permutation(1 << k)
+        want = st.copy()
+        O.apply_genperm(want, n, perm, diag, targets, ctrls)
+        sv = sv_from(st)
+        sv.apply_generalized_permutation(G.PermutationGate(perm, diag, tuple(targets), tuple(ctrls)))
+        _check(sv.amplitudes, want, dtype, exact=True)
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_swaps_many_pairs_bit_exact(dtype):
+    rng = np.random.default_rng(5)
+    for n in (2, 3, 7, 12, 16):
+        for npairs in range(1, n // 2 + 1):
+            bits = rng.permutation(n).tolist()
+            pairs = [(bits[2 * i], bits[2 * i + 1]) for i in range(npairs)]
+            st = random_state(n, rng, dtype)
+            sv = sv_from(st)
+            sv.swap_index_bits(pairs)
+            np.testing.assert_array_equal(sv.amplitudes, O.swap_index_bits(st, n, pairs))
+            sv.swap_index_bits(pairs)
+            np.testing.assert_array_equal(sv.amplitudes, st)
+            assert sv.bit_map == list(range(n))
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_reductions_vs_oracle(dtype):
+    rng = np.random.default_rng(9)
+    for n in (1, 2, 5, 11, 15):
+        st = random_state(n, rng, dtype)
+        sv = sv_from(st)
+        assert abs(sv.norm_squared() - 1.0) < 1e-5
+        for k in range(1, min(n, 10) + 1):
+            bits = rng.permutation(n)[:k].tolist()
+            np.testing.assert_allclose(sv.probabilities(bits), O.marginal(st.astype(np.complex128), n, bits), atol=1e-6)
+        for _ in range(4):
+            m = int(rng.integers(1, n + 1))
+            fac = tuple((int(q), str(rng.choice(list("IXYZ")))) for q in rng.permutation(n)[:m])
+            got = sv.expectation([G.PauliString(fac)])
+            want = O.expectation_pauli(st.astype(np.complex128), n, fac)
+            assert abs(got - want) < 1e-5
+        for kd in range(1, min(n, 6) + 1):
+            tq = tuple(int(q) for q in rng.permutation(n)[:kd])
+            a = rng.standard_normal((1 << kd, 1 << kd)) + 1j * rng.standard_normal((1 << kd, 1 << kd))
+            herm = (a + a.conj().T) / 2
+            got = sv.expectation(G.DenseGate(herm, tq, unitary=False))
+            want = O.expectation_dense(st.astype(np.complex128), n, herm, tq)
+            assert abs(got - want) < 1e-4 * max(1.0, abs(want))
+        np.testing.assert_array_equal(sv.amplitudes, st)
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_rotations_and_collapse_vs_oracle(dtype):
+    rng = np.random.default_rng(13)
+    for n in (1, 3, 8, 12):
+        st = random_state(n, rng, dtype)
+        for _ in range(3):
+            m = int(rng.integers(1, n + 1))
+            fac = tuple((int(q), str(rng.choice(list("XYZ")))) for q in rng.permutation(n)[:m])
+            theta, coef = float(rng.uniform(0, 6.3)), complex(np.exp(1j * rng.uniform(0, 6.3)))
+            sv = sv_from(st)
+            sv.apply_pauli_rotation(theta, G.PauliString(fac, coef))
+            want = st.copy()
+            O.pauli_rotation(want, n, theta, fac, coef)
+            np.testing.assert_allclose(sv.amplitudes, want, atol=10 * TOL[np.dtype(dtype)])
+        k = int(rng.integers(1, min(n, 4) + 1))
+        bits = rng.permutation(n)[:k].tolist()
+        r = float(rng.random())
+        sv = sv_from(st)
+        got = sv.measure(bits, r)
+        want_o, want = O.measure(st, n, bits, r)
+        assert got == want_o
+        np.testing.assert_allclose(sv.amplitudes, want, atol=10 * TOL[np.dtype(dtype)])
+
+
+def test_edge_cases_and_errors():
+    sv = StateVector(1)
+    sv.apply_generalized_permutation(G.x(0))
+    np.testing.assert_array_equal(sv.amplitudes, [0, 1])
+    sv.apply_generalized_permutation(G.PermutationGate([0, 1], [1, 1], (0,)))  # identity: no-op
+    np.testing.assert_array_equal(sv.amplitudes, [0, 1])
+    with pytest.raises(InvalidArgumentError):
+        sv.apply_matrix(G.h(3))
+    with pytest.raises(InvalidArgumentError):
+        StateVector(0)
+    with pytest.raises(InvalidArgumentError):
+        sv_from(np.zeros(2, dtype=complex)).measure([0], 0.5)
+    with pytest.raises(InvalidArgumentError):
+        sv.sample(0)
+    with pytest.raises(InvalidArgumentError):
+        sv.apply_pauli_rotation(0.1, G.PauliString(()))
+    with pytest.raises(InvalidArgumentError):
+        sv.probabilities([0, 0])
+    with pytest.raises(InvalidArgumentError):
+        sv.access([0, 0])
+    with pytest.raises(InvalidArgumentError):
+        sv.swap_index_bits([(0, 1)])
+    with pytest.raises(InvalidArgumentError):
+        StateVector(4).native.apply_matrix(np.eye(2), [7])  # C-ABI validation path
+    with pytest.raises(InvalidArgumentError):
+        SegmentedStateVector(4, 2).apply_gate_distributed(G.unitary(G.random_unitary(8, np.random.default_rng(0)), (0, 1, 2)))
+    # k == n dense and permutation gates
+    rng = np.random.default_rng(1)
+    for n in (1, 2, 3):
+        st = random_state(n, rng)
+        m = G.random_unitary(1 << n, rng)
+        sv = sv_from(st)
+        sv.apply_matrix(G.DenseGate(m, tuple(range(n))[::-1]))
+        want = st.copy()
+        O.apply_dense(want, n, m, list(range(n))[::-1])
+        np.testing.assert_allclose(sv.amplitudes, want, atol=1e-12)
+
+
+def test_raw_kernel_compat_functions():
+    from paper_2308_01999_b200 import statevec as S
+
+    rng = np.random.default_rng(4)
+    st = random_state(6, rng)
+    m = G.random_unitary(4, rng)
+    a = st.copy()
+    S.apply_dense_bits(a, 6, m, [1, 4], [(2, 1)])
+    b = st.copy()
+    O.apply_dense(b, 6, m, [1, 4], [(2, 1)])
+    np.testing.assert_allclose(a, b, atol=1e-12)
+    a = st.copy()
+    S.apply_pauli_product_bits(a, 6, [(0, "X"), (3, "Y"), (5, "Z")])
+    b = st.copy()
+    O.apply_pauli_product(b, 6, [(0, "X"), (3, "Y"), (5, "Z")])
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_allclose(S.marginal_probabilities_bits(st, 6, [5, 0]), O.marginal(st, 6, [5, 0]), atol=1e-12)
+
+
+def test_native_code_is_what_runs():
+    before = N.launch_count()
+    sv = StateVector(10, dtype=np.complex64)
+    sv.apply(G.h(3))
+    sv.apply(G.cx(3, 7))
+    sv.norm_squared()
+    assert N.launch_count() - before >= 3
