@@ -98,6 +98,8 @@ struct dsv_state {
   cudaStream_t stream = nullptr;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  void* gdata = nullptr;  // per-gate tables (stream-ordered reuse)
+  size_t gdata_bytes = 0;
   bool prof_on = false;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
@@ -120,6 +122,20 @@ int ensure_scratch(dsv_state* s, size_t bytes) {
   size_t want = std::max<size_t>(bytes, size_t(1) << 20);
   CK(cudaMalloc(&s->scratch, want));
   s->scratch_bytes = want;
+  return DSV_OK;
+}
+
+int ensure_gdata(dsv_state* s, size_t bytes) {
+  if (s->gdata_bytes >= bytes) return DSV_OK;
+  if (s->gdata) {
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaFree(s->gdata));
+    s->gdata = nullptr;
+    s->gdata_bytes = 0;
+  }
+  size_t want = std::max<size_t>(bytes, size_t(64) << 10);
+  CK(cudaMalloc(&s->gdata, want));
+  s->gdata_bytes = want;
   return DSV_OK;
 }
 
@@ -412,6 +428,7 @@ int dsv_state_destroy(dsv_state* s) {
   for (auto e : s->uev)
     if (e) cudaEventDestroy(e);
   if (s->scratch) cudaFree(s->scratch);
+  if (s->gdata) cudaFree(s->gdata);
   if (s->d) {
     if (s->ipc) cudaIpcCloseMemHandle(s->d);
     else if (s->owned) cudaFree(s->d);
@@ -604,6 +621,50 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
                        double(nactive) / double(D);
   bool is_diag = true;
   for (uint64_t j = 0; j < D; ++j) is_diag = is_diag && pn[j] == j;
+  const int kk = k + nctrl;
+  if (is_diag && kk <= (s->dtype == DSV_C64 ? kDiagStreamMaxBits : kDiagStreamMaxBits - 1)) {
+    // streaming path: one table over targets + controls, contiguous 16-B units
+    std::vector<int> B(gg.holes);  // sorted targets + controls (amp bits)
+    const uint64_t T = 1ull << kk;
+    const size_t es = amp_bytes(s->dtype);
+    std::vector<unsigned char> tab((es + 1) * T);
+    unsigned char* fl = tab.data() + es * T;
+    std::vector<int> pos_t(k), pos_c(nctrl);
+    for (int m = 0; m < k; ++m) pos_t[m] = int(std::find(B.begin(), B.end(), gg.tsorted[m]) - B.begin());
+    for (int c = 0; c < nctrl; ++c) pos_c[c] = int(std::find(B.begin(), B.end(), cb[c]) - B.begin());
+    for (uint64_t x = 0; x < T; ++x) {
+      bool ok = true;
+      for (int c = 0; c < nctrl; ++c) ok = ok && int((x >> pos_c[c]) & 1ull) == cv[c];
+      uint64_t j = 0;
+      for (int m = 0; m < k; ++m) j |= ((x >> pos_t[m]) & 1ull) << m;
+      if (s->dtype == DSV_C128) {
+        reinterpret_cast<cplx<double>*>(tab.data())[x] =
+            ok ? reinterpret_cast<const cplx<double>*>(dn.data())[j] : cplx<double>{1.0, 0.0};
+      } else {
+        reinterpret_cast<cplx<float>*>(tab.data())[x] =
+            ok ? reinterpret_cast<const cplx<float>*>(dn.data())[j] : cplx<float>{1.0f, 0.0f};
+      }
+      fl[x] = (ok && act[j]) ? 1 : 0;
+    }
+    // a 32-byte sector spans amp bits {0,1} (complex64) or {0} (complex128)
+    uint64_t smask = 0;
+    for (int m = 0; m < kk; ++m)
+      if (B[m] < (s->dtype == DSV_C64 ? 2 : 1)) smask |= 1ull << m;
+    for (uint64_t x = 0; x < T; ++x) {
+      bool touched = false;
+      for (uint64_t sub = smask;; sub = (sub - 1) & smask) {
+        touched = touched || (fl[x ^ sub] & 1);
+        if (!sub) break;
+      }
+      if (touched) fl[x] |= 2;
+    }
+    if (int rc = ensure_gdata(s, tab.size())) return rc;
+    CK(cudaMemcpyAsync(s->gdata, tab.data(), tab.size(), cudaMemcpyHostToDevice, s->stream));
+    ProfTok t = prof_start(s);
+    CKL(launch_diag_stream(s->dtype, s->nbits, kk, B.data(), s->gdata, s->d, s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
   if (is_diag) {
     // elementwise path: holes = control bits only, targets stay in the stream
     GateGeom cg = gg;

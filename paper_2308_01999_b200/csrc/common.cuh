@@ -85,6 +85,20 @@ __device__ __forceinline__ void cmul_numpy(R dr, R di, R ar, R ai, R& outr, R& o
 template <typename V> __device__ __forceinline__ V ldg_s(const V* p) { return __ldcs(p); }
 template <typename V> __device__ __forceinline__ void stg_s(V* p, const V& v) { __stcs(p, v); }
 
+// SM count of the current device (cached per device; persistent grids)
+inline int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
 // ---- block reductions (fixed order => run-to-run deterministic) ------------
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {

@@ -25,6 +25,12 @@ constexpr int kPermRegMaxK = 5;
 // tb = unit-space target bits (sorted), active[j] = entry j differs from 1
 cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb, const void* diag,
                         const unsigned char* active, void* sv, cudaStream_t st);
+// streaming diagonal over a table of kk <= kDiagStreamMaxBits bits (targets and
+// controls folded in); d_tab = [cplx d[2^kk]][uint8 flags[2^kk]] in device
+// memory, flags bit0 = entry active, bit1 = its 32-byte sector is touched
+constexpr int kDiagStreamMaxBits = 12;
+cudaError_t launch_diag_stream(int dtype, int nbits, int kk, const int* amp_bits, const void* d_tab,
+                               void* sv, cudaStream_t st);
 cudaError_t launch_perm_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs_in,
                             const uint64_t* offs_out, const void* diag, uint64_t active,
                             void* sv, cudaStream_t st);

@@ -149,33 +149,39 @@ k_diag(const __grid_constant__ DiagP<typename VT::R> p, typename VT::V* __restri
     sa[j] = p.active[j];
   }
   __syncthreads();
-  const uint64_t w0 = uint64_t(blockIdx.x) * (uint64_t(blockDim.x) * ITEMS) + threadIdx.x;
-  V v[ITEMS];
-  uint64_t idx[ITEMS];
-  int jj[ITEMS];
-  bool on[ITEMS];
+  // persistent grid-stride over chunks of blockDim*ITEMS units: the table
+  // prologue is paid once per CTA, not once per 16 KB of traffic
+  const uint64_t per_chunk = uint64_t(blockDim.x) * ITEMS;
+  const uint64_t nchunks = (p.g.nwork + per_chunk - 1) / per_chunk;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t w0 = c * per_chunk + threadIdx.x;
+    V v[ITEMS];
+    uint64_t idx[ITEMS];
+    int jj[ITEMS];
+    bool on[ITEMS];
 #pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    const uint64_t w = w0 + uint64_t(it) * blockDim.x;
-    idx[it] = expand(p.g, w);
-    int j = 0;
-    for (int m = 0; m < p.k; ++m) j |= int((idx[it] >> p.tb[m]) & 1ull) << m;
-    jj[it] = j;
-    on[it] = (w < p.g.nwork) && sa[j];
-    if (on[it]) v[it] = ldg_s(sv + idx[it]);
-  }
-#pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    if (!on[it]) continue;
-    const cplx<R> d = sd[jj[it]];
-#pragma unroll
-    for (int l = 0; l < VT::L; ++l) {
-      R ar, ai, orr, oi;
-      VT::get(v[it], l, ar, ai);
-      cmul_numpy(d.x, d.y, ar, ai, orr, oi);
-      VT::set(v[it], l, orr, oi);
+    for (int it = 0; it < ITEMS; ++it) {
+      const uint64_t w = w0 + uint64_t(it) * blockDim.x;
+      idx[it] = expand(p.g, w);
+      int j = 0;
+      for (int m = 0; m < p.k; ++m) j |= int((idx[it] >> p.tb[m]) & 1ull) << m;
+      jj[it] = j;
+      on[it] = (w < p.g.nwork) && sa[j];
+      if (on[it]) v[it] = ldg_s(sv + idx[it]);
     }
-    stg_s(sv + idx[it], v[it]);
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      if (!on[it]) continue;
+      const cplx<R> d = sd[jj[it]];
+#pragma unroll
+      for (int l = 0; l < VT::L; ++l) {
+        R ar, ai, orr, oi;
+        VT::get(v[it], l, ar, ai);
+        cmul_numpy(d.x, d.y, ar, ai, orr, oi);
+        VT::set(v[it], l, orr, oi);
+      }
+      stg_s(sv + idx[it], v[it]);
+    }
   }
 }
 
@@ -194,8 +200,10 @@ static cudaError_t diag_t(const Geom& g, int k, const int* tb, const void* diag,
     p.active[j] = active[j];
   }
   const uint64_t per_block = 256ull * ITEMS;
-  const uint64_t blocks = (g.nwork + per_block - 1) / per_block;
+  uint64_t blocks = (g.nwork + per_block - 1) / per_block;
   if (blocks == 0) return cudaSuccess;
+  const uint64_t cap = uint64_t(device_sm_count()) * 8;  // 8 x 256 threads resident per SM
+  if (blocks > cap) blocks = cap;
   k_diag<VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
   return cudaGetLastError();
 }

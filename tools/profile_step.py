@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""One benchmark step (reset + fused QFT-n circuit) with nothing else, for ncu:
+
+    ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/launches.csv python tools/profile_step.py --n 33
+    ncu --set full --clock-control none --import-source on -k regex:k_diag -s 10 -c 2 \
+        -o gpurun_out/prof_diag python tools/profile_step.py --n 28
+"""
+
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from paper_2308_01999_b200.circuits import gen_qft, to_gates  # noqa: E402
+from paper_2308_01999_b200.fusion import FusionConfig, fuse  # noqa: E402
+from paper_2308_01999_b200.statevec import StateVector  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=33)
+    ap.add_argument("--dtype", default="c64")
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--fusion", default="5,6")
+    args = ap.parse_args()
+    k, d = (int(x) for x in args.fusion.split(","))
+    fc = fuse(to_gates(gen_qft(args.n)), FusionConfig(k, d))
+    sv = StateVector(args.n, dtype=np.complex64 if args.dtype == "c64" else np.complex128)
+    for _ in range(args.steps):
+        sv.native.set_basis(0)
+        for g in fc.gates:
+            sv.apply(g)
+    sv.native.sync()
+    print(f"ran {args.steps} step(s) of {len(fc)} fused ops at n={args.n}")
+
+
+if __name__ == "__main__":
+    main()
