@@ -87,6 +87,14 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
 int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag,
                       const int32_t* targets, int k, const int32_t* ctrl_bits,
                       const int32_t* ctrl_vals, int nctrl);
+/* Fused window of the opt-in fold fuser (fusion_fold.py; extension of the
+ * reference's fused gates, fusion.py:97-121): dense matrix on `targets`
+ * applied after the diagonal exp(i (sum_x theta_x [target cross_t[x]] [bit cross_b[x]]
+ * + sum_y out_theta[y] [bit out_b[y]])), cross_t indexing `targets`, cross_b /
+ * out_b physical bits outside the targets.  k <= 5, no controls. */
+int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* targets, int k,
+                            const int32_t* cross_t, const int32_t* cross_b, const double* cross_theta,
+                            int ncross, const int32_t* out_b, const double* out_theta, int nout);
 /* replaces StateVector.apply_pauli_rotation, statevec.py:196-207 (copy-free):
  * psi <- cos(theta/2) psi - i sin(theta/2) coef (P psi); paulis[i] in "IXYZ" */
 int dsv_apply_pauli_rotation(dsv_state* s, double theta, double coef_re, double coef_im,

@@ -53,6 +53,7 @@ SIGNATURES: dict[str, list] = {
     "dsv_copy": [_vp, _vp],
     "dsv_apply_matrix": [_vp, _vp, _i32p, _int, _i32p, _i32p, _int],
     "dsv_apply_genperm": [_vp, _i64p, _vp, _i32p, _int, _i32p, _i32p, _int],
+    "dsv_apply_matrix_phased": [_vp, _vp, _i32p, _int, _i32p, _i32p, _dp, _int, _i32p, _dp, _int],
     "dsv_apply_pauli_rotation": [_vp, _dbl, _dbl, _dbl, _i32p, C.c_char_p, _int],
     "dsv_apply_pauli_product": [_vp, _i32p, C.c_char_p, _int],
     "dsv_swap_index_bits": [_vp, _i32p, _int],
@@ -242,6 +243,19 @@ class NativeState:
         cb, cbp = i32([b for b, _ in controls])
         cv, cvp = i32([v for _, v in controls])
         call("dsv_apply_matrix", self._h, ptr(m), tp, len(t), cbp, cvp, len(cb))
+
+    def apply_matrix_phased(self, matrix, targets, cross=(), outside=()) -> None:
+        """cross: (target index m, outside bit, theta); outside: (bit, theta)."""
+        m = np.ascontiguousarray(matrix, dtype=self.dtype)
+        t, tp = i32(targets)
+        ct, ctp = i32([c[0] for c in cross])
+        cb, cbp = i32([c[1] for c in cross])
+        cth = np.ascontiguousarray([float(c[2]) for c in cross], dtype=np.float64)
+        ob, obp = i32([o[0] for o in outside])
+        oth = np.ascontiguousarray([float(o[1]) for o in outside], dtype=np.float64)
+        call("dsv_apply_matrix_phased", self._h, ptr(m), tp, len(t), ctp, cbp,
+             cth.ctypes.data_as(_dp) if cth.size else None, len(ct), obp,
+             oth.ctypes.data_as(_dp) if oth.size else None, len(ob))
 
     def apply_genperm(self, perm, diag, targets, controls=()) -> None:
         p, pp = i64(perm)

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -29,6 +30,13 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+// The shared-memory tile path for low-target dense gates is opt-in
+// (DSV_ENABLE_TILE=1): the sweep shows the register path ahead at every
+// low-target position so far (profiles/sweep_r1_tile_ab.json).
+const bool g_disable_tile = [] {
+  const char* e = std::getenv("DSV_ENABLE_TILE");
+  return !(e && e[0] == '1');
+}();
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -528,6 +536,58 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   DeviceGuard g(s->device);
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * std::ldexp(1.0, s->nbits - nctrl);
   const uint64_t D = 1ull << k;
+  int nlow = 0;
+  for (int m = 0; m < k; ++m) nlow += gg.tsorted[m] < (s->dtype == DSV_C64 ? 4 : 3);
+  if (k >= 2 && k <= 5 && nlow >= 2 && s->nbits >= 14 && !g_disable_tile) {
+    // low targets: shared-memory tiles, 2^kh rows x 2^T contiguous amplitudes
+    int T = 10, kh = 0;
+    for (; T >= 6; --T) {
+      kh = 0;
+      for (int m = 0; m < k; ++m) kh += gg.tsorted[m] >= T;
+      if (T + kh <= 12) break;
+    }
+    TileDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.T = T;
+    d.kh = kh;
+    std::vector<int> holes;
+    for (int b = 0; b < T; ++b) holes.push_back(b);
+    std::vector<int> high;
+    for (int m = 0; m < k; ++m)
+      if (gg.tsorted[m] >= T) high.push_back(gg.tsorted[m]);
+    uint64_t setm = 0;
+    for (int c = 0; c < nctrl; ++c) {
+      if (cb[c] >= T) {
+        holes.push_back(cb[c]);
+        if (cv[c]) setm |= 1ull << cb[c];
+      } else {
+        d.cmask |= 1u << cb[c];
+        if (cv[c]) d.cval |= 1u << cb[c];
+      }
+    }
+    for (int b : high) holes.push_back(b);
+    std::sort(holes.begin(), holes.end());
+    if (int rc = make_geom(s->nbits, holes, setm, &d.g)) return rc;
+    for (int r = 0; r < (1 << kh); ++r) {
+      uint64_t o = 0;
+      for (int i = 0; i < kh; ++i) o |= uint64_t((r >> i) & 1) << high[i];
+      d.hoff[r] = o;
+    }
+    int hi_i = 0;
+    for (int m = 0; m < k; ++m) d.lt[m] = gg.tsorted[m] < T ? gg.tsorted[m] : T + hi_i++;
+    ProfTok t = prof_start(s);
+    if (s->dtype == DSV_C128) {
+      std::vector<cplx<double>> m;
+      canon_matrix<double>(gg, matrix, m);
+      CKL(launch_dense_tile(s->dtype, k, d, m.data(), s->d, s->stream), 1);
+    } else {
+      std::vector<cplx<float>> m;
+      canon_matrix<float>(gg, matrix, m);
+      CKL(launch_dense_tile(s->dtype, k, d, m.data(), s->d, s->stream), 1);
+    }
+    prof_stop(s, t, PC_DENSE, bytes);
+    return DSV_OK;
+  }
   if (k <= kDenseRegMaxK) {
     UnitView uv;
     // float4 pairs only while 2^k x 2 amplitudes fit the register budget
@@ -576,6 +636,85 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   prof_stop(s, t, PC_DENSE_GENERIC, bytes);
   // the host staging vectors die at return: make the copies complete first
   CK(cudaStreamSynchronize(s->stream));
+  return DSV_OK;
+}
+
+int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* targets, int k,
+                            const int32_t* cross_t, const int32_t* cross_b, const double* cross_theta,
+                            int ncross, const int32_t* out_b, const double* out_theta, int nout) {
+  if (int rc = check_state(s)) return rc;
+  if (!matrix) return fail(DSV_EINVAL, "null matrix");
+  if (k < 1 || k > kDenseRegMaxK) return fail(DSV_EUNSUPPORTED, "phased window arity %d outside [1, 5]", k);
+  if (ncross < 0 || nout < 0) return fail(DSV_EINVAL, "negative term count");
+  GateGeom gg;
+  if (int rc = validate_gate(s, targets, k, nullptr, nullptr, 0, &gg)) return rc;
+  uint64_t tmask = 0;
+  for (int m = 0; m < k; ++m) tmask |= 1ull << targets[m];
+  // sorted position of caller target index m
+  std::vector<int> newpos(k);
+  for (int mp = 0; mp < k; ++mp) newpos[gg.order[mp]] = mp;
+  struct Term { int slot, bit; double th; };
+  std::vector<Term> terms;
+  for (int x = 0; x < ncross; ++x) {
+    if (cross_t[x] < 0 || cross_t[x] >= k) return fail(DSV_EINVAL, "cross term target index %d out of range", cross_t[x]);
+    const int b = cross_b[x];
+    if (b < 0 || b >= s->nbits || (tmask >> b & 1)) return fail(DSV_EINVAL, "cross term bit %d must be an outside bit", b);
+    terms.push_back({newpos[cross_t[x]], b, cross_theta[x]});
+  }
+  for (int y = 0; y < nout; ++y) {
+    const int b = out_b[y];
+    if (b < 0 || b >= s->nbits || (tmask >> b & 1)) return fail(DSV_EINVAL, "outside term bit %d must be an outside bit", b);
+    terms.push_back({k, b, out_theta[y]});
+  }
+  DeviceGuard g(s->device);
+  UnitView uv;
+  if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;
+  // active index bytes and the [nchunk][256][k+1] tables
+  int chunk_of_byte[8];
+  PhasedDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.g = uv.g;
+  for (int j = 0; j < (1 << k); ++j) d.offs[j] = uv.offs[j];
+  for (int c = 0; c < 8; ++c) chunk_of_byte[c] = -1;
+  for (const Term& t : terms) {
+    const int c = t.bit / 8;
+    if (chunk_of_byte[c] < 0) {
+      chunk_of_byte[c] = d.nchunk;
+      d.chunk_shift[d.nchunk++] = 8 * c;
+    }
+  }
+  const int S = k + 1;
+  const size_t nt = size_t(std::max(d.nchunk, 1)) * 256 * S;
+  if (d.nchunk == 0) {  // no outside terms: still valid (plain dense), keep one zero chunk
+    d.nchunk = 1;
+    d.chunk_shift[0] = 0;
+  }
+  std::vector<double> tab(nt, 0.0);
+  for (const Term& t : terms) {
+    const int ci = chunk_of_byte[t.bit / 8];
+    const int bb = t.bit % 8;
+    for (int v = 0; v < 256; ++v)
+      if ((v >> bb) & 1) tab[(size_t(ci) * 256 + v) * S + t.slot] += t.th;
+  }
+  const size_t es = s->dtype == DSV_C128 ? 8 : 4;
+  std::vector<unsigned char> raw(nt * es);
+  if (s->dtype == DSV_C128) std::memcpy(raw.data(), tab.data(), nt * 8);
+  else
+    for (size_t i = 0; i < nt; ++i) reinterpret_cast<float*>(raw.data())[i] = float(tab[i]);
+  if (int rc = ensure_gdata(s, raw.size())) return rc;
+  CK(cudaMemcpyAsync(s->gdata, raw.data(), raw.size(), cudaMemcpyHostToDevice, s->stream));
+  const double bytes = 2.0 * double(amp_bytes(s->dtype)) * double(namps(s));
+  ProfTok t = prof_start(s);
+  if (s->dtype == DSV_C128) {
+    std::vector<cplx<double>> m;
+    canon_matrix<double>(gg, matrix, m);
+    CKL(launch_dense_phased(s->dtype, uv.mode, k, d, m.data(), s->gdata, s->d, s->stream), 1);
+  } else {
+    std::vector<cplx<float>> m;
+    canon_matrix<float>(gg, matrix, m);
+    CKL(launch_dense_phased(s->dtype, uv.mode, k, d, m.data(), s->gdata, s->d, s->stream), 1);
+  }
+  prof_stop(s, t, PC_DENSE, bytes);
   return DSV_OK;
 }
 

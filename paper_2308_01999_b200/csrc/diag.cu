@@ -20,6 +20,7 @@
 // with at least one active entry are read and written whole (inactive
 // amplitudes are written back bit-identical), so the DRAM never sees a
 // partial-sector write.  The product is NumPy's FMA form => bit-exact.
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -34,8 +35,8 @@ struct DiagStreamP {
   int ub[kDiagStreamMaxBits];  // unit-space bit of table bit m (-1: lane bit)
 };
 
-template <typename R, int L, int ITEMS>
-__global__ void __launch_bounds__(256, 4)
+template <typename R, int L, int ITEMS, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 k_diag_stream(const __grid_constant__ DiagStreamP p, const unsigned char* __restrict__ tab,
               typename std::conditional<L == 2, float4, double2>::type* __restrict__ sv) {
   using V = typename std::conditional<L == 2, float4, double2>::type;
@@ -126,6 +127,22 @@ k_diag_stream(const __grid_constant__ DiagStreamP p, const unsigned char* __rest
   }
 }
 
+template <typename R, int L, int ITEMS, int MINB>
+static cudaError_t diag_stream_go(const DiagStreamP& p, const void* d_tab, void* sv, size_t smem,
+                                  cudaStream_t st) {
+  using V = typename std::conditional<L == 2, float4, double2>::type;
+  const uint64_t per_block = 256ull * ITEMS;
+  uint64_t blocks = (p.nunits + per_block - 1) / per_block;
+  const uint64_t cap = uint64_t(device_sm_count()) * MINB;  // persistent: MINB x 256 threads per SM
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_diag_stream<R, L, ITEMS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_diag_stream<R, L, ITEMS, MINB><<<unsigned(blocks), 256, smem, st>>>(
+      p, static_cast<const unsigned char*>(d_tab), static_cast<V*>(sv));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_diag_stream(int dtype, int nbits, int kk, const int* amp_bits, const void* d_tab,
                                void* sv, cudaStream_t st) {
   DiagStreamP p;
@@ -138,26 +155,19 @@ cudaError_t launch_diag_stream(int dtype, int nbits, int kk, const int* amp_bits
     p.ub[m] = amp_bits[m] - shift;
     if (p.ub[m] < 0) p.lane_m = m;
   }
-  constexpr int ITEMS = 8;
-  const uint64_t per_block = 256ull * ITEMS;
-  uint64_t blocks = (p.nunits + per_block - 1) / per_block;
-  const uint64_t cap = uint64_t(device_sm_count()) * 4;  // 4 x 256 threads resident per SM (launch bounds)
-  if (blocks > cap) blocks = cap;
-  if (blocks == 0) blocks = 1;
+  // variant: DSV_DIAG_VARIANT=0 -> 8 units/thread, 4 CTAs/SM; 1 -> 4 units, 8 CTAs/SM
+  static const int variant = [] {
+    const char* e = std::getenv("DSV_DIAG_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
   const size_t es = dtype == 1 ? 16 : 8;
   const size_t smem = (es + 1) << kk;
-  if (dtype == 1) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_diag_stream<double, 1, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    k_diag_stream<double, 1, ITEMS><<<unsigned(blocks), 256, smem, st>>>(
-        p, static_cast<const unsigned char*>(d_tab), static_cast<double2*>(sv));
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_diag_stream<float, 2, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    k_diag_stream<float, 2, ITEMS><<<unsigned(blocks), 256, smem, st>>>(
-        p, static_cast<const unsigned char*>(d_tab), static_cast<float4*>(sv));
+  if (variant == 0) {
+    if (dtype == 1) return diag_stream_go<double, 1, 8, 4>(p, d_tab, sv, smem, st);
+    return diag_stream_go<float, 2, 8, 4>(p, d_tab, sv, smem, st);
   }
-  return cudaGetLastError();
+  if (dtype == 1) return diag_stream_go<double, 1, 4, 8>(p, d_tab, sv, smem, st);
+  return diag_stream_go<float, 2, 4, 8>(p, d_tab, sv, smem, st);
 }
 
 }  // namespace dsv

@@ -15,6 +15,26 @@ enum Mode { MODE_SCALAR = 0, MODE_VEC2 = 1 };  // VEC2: complex64 with index bit
 constexpr int kDenseRegMaxK = 5;
 cudaError_t launch_dense_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs,
                              const void* matrix, void* sv, cudaStream_t st);
+// k <= 5 dense gate preceded by an outside-coupled phase polynomial
+// (tab: [nchunk][256][k+1] of the state's real type, in device memory)
+struct PhasedDesc {
+  Geom g;
+  int nchunk;
+  int chunk_shift[8];
+  uint64_t offs[32];
+};
+cudaError_t launch_dense_phased(int dtype, int mode, int k, const PhasedDesc& d, const void* matrix,
+                                const void* d_tab, void* sv, cudaStream_t st);
+// k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem
+struct TileDesc {
+  Geom g;              // tile bases (holes: bits [0,T), high targets, controls >= T)
+  int T, kh;
+  uint64_t hoff[32];   // amp offset of tile row r
+  int lt[5];           // tile-local bit of sorted target m
+  uint32_t cmask, cval;
+};
+cudaError_t launch_dense_tile(int dtype, int k, const TileDesc& d, const void* matrix, void* sv,
+                              cudaStream_t st);
 // any k <= 10: one CTA per group through shared memory, matrix transposed in HBM
 cudaError_t launch_dense_generic(int dtype, int k, const Geom& g, const uint64_t* d_offs,
                                  const void* d_matrix_t, void* sv, cudaStream_t st);

@@ -171,7 +171,9 @@ class DistributedStateVector:
         self.rank = self.comm.rank
         self.dtype = np.dtype(dtype)
         if segment_factory is None:
-            dev = getattr(self.comm, "local_rank", self.rank)
+            from . import _native as N
+
+            dev = getattr(self.comm, "local_rank", self.rank) % max(1, N.device_count())
             self.seg = NvlinkSegment(self.comm, self.local_bits, self.dtype, dev)
         else:
             self.seg = segment_factory(self.comm, self.local_bits, self.dtype)

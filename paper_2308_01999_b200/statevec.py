@@ -141,11 +141,32 @@ class StateVector:
         return self.access(self.bit_map)
 
     # -- Table I primitives -----------------------------------------------------------
-    def apply(self, g: Gate) -> None:
+    def apply(self, g) -> None:
         if isinstance(g, PermutationGate):
             self.apply_generalized_permutation(g)
-        else:
+        elif isinstance(g, DenseGate):
             self.apply_matrix(g)
+        else:
+            self._apply_folded(g)
+
+    def _apply_folded(self, op) -> None:
+        """Ops of the opt-in fold fuser (fusion_fold.py): phased dense windows
+        and SWAP-as-relabel (bit_map only, no data movement)."""
+        from .fusion_fold import PhasedDenseGate, QubitSwap
+
+        if isinstance(op, QubitSwap):
+            self._bits([op.a, op.b])
+            self.bit_map[op.a], self.bit_map[op.b] = self.bit_map[op.b], self.bit_map[op.a]
+            return
+        if not isinstance(op, PhasedDenseGate):
+            raise InvalidArgumentError(f"cannot apply {type(op).__name__}")
+        bits = self._bits(op.targets)
+        pos = {q: m for m, q in enumerate(op.targets)}
+        cross = [(pos[a], self._bits([b])[0], t) for a, b, t in op.cross]
+        outside = [(self._bits([b])[0], t) for b, t in op.outside]
+        self._sync_in()
+        self._dev.apply_matrix_phased(np.asarray(op.matrix, dtype=self.dtype), bits, cross, outside)
+        self._mutated()
 
     def apply_matrix(self, g: DenseGate) -> None:
         """Dense gate, matrix cast to the state dtype (statevec.py:177-184)."""

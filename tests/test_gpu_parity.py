@@ -237,6 +237,31 @@ def test_dense_all_arities_vs_oracle(dtype, k):
 
 
 @pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_dense_low_targets_tile_path_vs_oracle(dtype, k):
+    """n >= 14 with >= 2 low targets takes the shared-memory tile kernel."""
+    rng = np.random.default_rng(300 + k)
+    n = 16
+    cases = [
+        list(range(k)),                                   # all low
+        [0, 1] + [int(x) for x in rng.choice(np.arange(11, n), size=k - 2, replace=False)],  # low + high rows
+        [1, 3] + list(range(6, 6 + k - 2)),               # low + inside-row
+    ]
+    for targets in cases:
+        for ctrls in ([], [(max(targets) + 1 if max(targets) + 1 < n else 2 if 2 not in targets else 4, 1)],
+                      [(q, int(rng.integers(0, 2))) for q in rng.permutation([q for q in range(n) if q not in targets])[:2]]):
+            ctrls = [(int(q), int(v)) for q, v in ctrls if q not in targets]
+            st = random_state(n, rng, dtype)
+            m = G.random_unitary(1 << k, rng)
+            perm_t = [int(x) for x in rng.permutation(targets)]
+            want = st.copy()
+            O.apply_dense(want, n, m, perm_t, ctrls)
+            sv = sv_from(st)
+            sv.apply_matrix(G.DenseGate(m, tuple(perm_t), tuple(ctrls)))
+            _check(sv.amplitudes, want, dtype, exact=False)
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
 @pytest.mark.parametrize("k", list(range(1, 9)))
 def test_genperm_and_diag_all_arities_bit_exact(dtype, k):
     rng = np.random.default_rng(200 + k)
