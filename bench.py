@@ -54,14 +54,29 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
-def workload():
-    from paper_2308_01999_b200.circuits import gen_qft, to_gates
+FOLD_K = 4  # fold fuser window size (<= 5 per the config); k=4 is HBM-bound on CUDA cores
+
+
+def fuse_ops(gates, fusion: str):
+    """'fold': the engine's phase-folding fuser (fusion_fold.py, windows of
+    <= FOLD_K qubits, SWAPs as relabels); 'reference': the reference's own
+    FusionConfig(5, 6) windows (fusion.py, 152 ops at n=33)."""
+    if fusion == "fold":
+        from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+        return fuse_fold(gates, FOLD_K).ops
     from paper_2308_01999_b200.fusion import FusionConfig, fuse
+
+    return fuse(gates, FusionConfig(*FUSION)).gates
+
+
+def workload(fusion: str = "fold"):
+    from paper_2308_01999_b200.circuits import gen_qft, to_gates
 
     gates = to_gates(gen_qft(N_QUBITS))
     t0 = time.perf_counter()
-    fc = fuse(gates, FusionConfig(*FUSION))
-    return gates, fc, time.perf_counter() - t0
+    ops = fuse_ops(gates, fusion)
+    return gates, ops, time.perf_counter() - t0
 
 
 # ---- clocks sampler ------------------------------------------------------------------------
@@ -146,8 +161,8 @@ def cpu_sample(nq: int, max_ops: int | None = None) -> dict:
         O.apply_gate(amps, nq, g)
     dt = time.perf_counter() - t0
     per_op = dt / len(ops)
-    _, fc33, _ = workload()
-    t33 = per_op * (1 << (N_QUBITS - nq)) * len(fc33)
+    _, ops33, _ = workload("reference")
+    t33 = per_op * (1 << (N_QUBITS - nq)) * len(ops33)
     return {"value": 577.0 / t33, "unit": "gates/s", "seconds": dt, "ops": len(ops), "per_op_s": per_op,
             "t33_s": t33}
 
@@ -180,7 +195,8 @@ def run_reference(args) -> None:
         "metric": METRIC, "value": v, "unit": "gates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c64", "data": "synthetic (QFT circuit from |0>)",
-        "config": {"workload": "qft33_c64_fused_k5_d6", "n_qubits": N_QUBITS, "fusion": list(FUSION)},
+        "config": {"workload": "qft33_c64_fused_k5", "n_qubits": N_QUBITS,
+                   "fusion": f"reference FusionConfig{FUSION} (the reference's own fuser)"},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": "gates/s", "cores": cpu_cores(), "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -208,8 +224,8 @@ def gate_payload_bytes(gates, itemsize: int) -> int:
     for g in gates:
         if isinstance(g, PermutationGate):
             b += g.diagonal.size * itemsize + g.permutation.size * 8
-        else:
-            b += g.matrix.size * itemsize
+        elif hasattr(g, "matrix"):
+            b += g.matrix.size * itemsize + 16 * (len(getattr(g, "cross", ())) + len(getattr(g, "outside", ())))
     return b
 
 
@@ -218,15 +234,15 @@ def run_single(args) -> None:
     from paper_2308_01999_b200.statevec import StateVector
 
     dev = N.default_device()
-    gates, fc, fuse_s = workload()
-    ops = fc.gates
+    gates, ops, fuse_s = workload(args.fusion)
     st = StateVector(N_QUBITS, dtype=np.complex64, device=dev)
     nat = st.native
-    mats = [(np.asarray(g.matrix if hasattr(g, "matrix") else g.diagonal, dtype=np.complex64)) for g in ops]
+    ident = list(range(N_QUBITS))
 
-    def step():
+    def step(op_list=ops):
         nat.set_basis(0)
-        for g in ops:
+        st.bit_map = list(ident)
+        for g in op_list:
             st.apply(g)
 
     for _ in range(args.warmup):
@@ -264,18 +280,24 @@ def run_single(args) -> None:
     kernels = {k: {"count": v["count"] // args.steps, "ms_per_step": v["ms"] / args.steps,
                    "GB_per_s": (v["bytes"] / (v["ms"] / 1000.0) / 1e9) if v["ms"] else None}
                for k, v in prof.items()}
+    # the same state, the reference fuser's 152 windows (drop-in fusion semantics)
+    ref_ops = fuse_ops(gates, "reference") if args.fusion == "fold" else ops
+    step(ref_ops)
+    nat.event_record(2)
+    step(ref_ops)
+    nat.event_record(3)
+    ref_ms = nat.event_elapsed(2, 3)
     del st, nat
 
     # e2e through the public API: fuse on the host, allocate, run, read back probabilities
-    from paper_2308_01999_b200.fusion import FusionConfig, fuse
     from paper_2308_01999_b200.statevec import run_circuit_sv
 
     e2e_times = []
     d2h = 0
     for i in range(max(1, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
-        f2 = fuse(gates, FusionConfig(*FUSION))
-        sv = run_circuit_sv(f2.gates, N_QUBITS, dtype=np.complex64, device=dev)
+        f2 = fuse_ops(gates, args.fusion)
+        sv = run_circuit_sv(f2, N_QUBITS, dtype=np.complex64, device=dev)
         p = sv.probabilities([0, 1, 2, 3])
         d2h = p.nbytes
         del sv
@@ -283,7 +305,7 @@ def run_single(args) -> None:
         if i > 0:  # first iteration is the e2e warm-up
             e2e_times.append(dt)
     e2e_s = statistics.median(e2e_times)
-    h2d = gate_payload_bytes(fc.gates, 8)
+    h2d = gate_payload_bytes(ops, 8)
 
     cpu = None
     if not args.skip_cpu:
@@ -300,8 +322,14 @@ def run_single(args) -> None:
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": value / PUBLISHED_1GPU_GATES_PER_S, "dtype": "c64",
         "data": "synthetic (QFT-33 circuit generated on the host, state starts at |0>)",
-        "config": {"workload": "qft33_c64_fused_k5_d6", "n_qubits": N_QUBITS, "circuit_gates": len(gates),
-                   "fused_ops": len(ops), "fusion": list(FUSION), "fuse_host_s": fuse_s,
+        "config": {"workload": "qft33_c64_fused_k5", "n_qubits": N_QUBITS, "circuit_gates": len(gates),
+                   "fused_ops": len(ops), "fuse_host_s": fuse_s,
+                   "fusion": (f"fold: dense windows <= {FOLD_K} qubits with controlled-phase folding, "
+                              "SWAP as relabel (fusion_fold.py)") if args.fusion == "fold"
+                   else f"reference FusionConfig{FUSION}",
+                   "data_passes": sum(1 for o in ops if hasattr(o, "matrix") or hasattr(o, "diagonal")),
+                   "reference_fuser_ops": len(ref_ops),
+                   "reference_fuser_gates_per_s": len(gates) / (ref_ms / 1000.0),
                    "l2": "state 64 GiB >> 126 MB L2 (no flush needed)", "parallelism": "single segment",
                    "vs_baseline_ref": "qsim-mgpu 1xH100 QFT-33 k=5: 577 gates/1.21 s (PAPER.md:285-288)"},
         "fused_ops_per_s": len(ops) / (ms_step / 1000.0),
@@ -325,6 +353,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--fusion", default="fold", choices=["fold", "reference"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -82,11 +82,13 @@ struct DeviceGuard {
 
 enum ProfClass {
   PC_DENSE = 0, PC_DENSE_GENERIC, PC_PERM, PC_PERM_GENERIC, PC_SWAP, PC_REDUCE,
-  PC_EXPECT, PC_PAULI, PC_COLLAPSE, PC_EXCHANGE, PC_ACCESS, PC_SAMPLE
+  PC_EXPECT, PC_PAULI, PC_COLLAPSE, PC_EXCHANGE, PC_ACCESS, PC_SAMPLE,
+  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE
 };
 const char* kProfNames[DSV_PROF_NCLASS] = {
     "dense", "dense_generic", "genperm", "genperm_generic", "swap_bits", "reduce",
-    "expect", "pauli", "collapse", "exchange", "access", "sample"};
+    "expect", "pauli", "collapse", "exchange", "access", "sample",
+    "dense_phased", "diag", "dense_tile", ""};
 
 struct ProfRec {
   int cls;
@@ -585,7 +587,7 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
       canon_matrix<float>(gg, matrix, m);
       CKL(launch_dense_tile(s->dtype, k, d, m.data(), s->d, s->stream), 1);
     }
-    prof_stop(s, t, PC_DENSE, bytes);
+    prof_stop(s, t, PC_DENSE_TILE, bytes);
     return DSV_OK;
   }
   if (k <= kDenseRegMaxK) {
@@ -714,7 +716,7 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
     canon_matrix<float>(gg, matrix, m);
     CKL(launch_dense_phased(s->dtype, uv.mode, k, d, m.data(), s->gdata, s->d, s->stream), 1);
   }
-  prof_stop(s, t, PC_DENSE, bytes);
+  prof_stop(s, t, PC_DENSE_PHASED, bytes);
   return DSV_OK;
 }
 
@@ -801,7 +803,7 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
     CK(cudaMemcpyAsync(s->gdata, tab.data(), tab.size(), cudaMemcpyHostToDevice, s->stream));
     ProfTok t = prof_start(s);
     CKL(launch_diag_stream(s->dtype, s->nbits, kk, B.data(), s->gdata, s->d, s->stream), 1);
-    prof_stop(s, t, PC_PERM, bytes);
+    prof_stop(s, t, PC_DIAG, bytes);
     return DSV_OK;
   }
   if (is_diag) {

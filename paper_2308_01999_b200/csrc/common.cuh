@@ -12,6 +12,7 @@
 // bits are free.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define DSV_MAX_GEOM_SEGS 41  // DSV_MAX_BITS holes + 1
@@ -84,6 +85,92 @@ __device__ __forceinline__ void cmul_numpy(R dr, R di, R ar, R ai, R& outr, R& o
 // every amplitude is touched once per pass.
 template <typename V> __device__ __forceinline__ V ldg_s(const V* p) { return __ldcs(p); }
 template <typename V> __device__ __forceinline__ void stg_s(V* p, const V& v) { __stcs(p, v); }
+
+// y = M x for one amplitude group held in registers (L lanes = groups per
+// unit), streamed out row by row.  Complex products in the 3-multiplication
+// (Gauss) form: with a + ib = M[r][c] and x + iy = x_c,
+//   re = P - Q,  im = S - P - Q,  P = sum a x,  Q = sum b y,  S = sum (a+b)(x+y)
+// — 3 FMAs per term instead of 4 (k >= 4 complex64 gates are FMA-bound on the
+// CUDA cores).  m and msum (= a + b) live in the kernel-parameter constant bank.
+template <int D, class VT>
+__device__ __forceinline__ void matvec3m_store(const cplx<typename VT::R>* __restrict__ m,
+                                               const typename VT::R* __restrict__ msum,
+                                               const typename VT::V (&in)[D], typename VT::V* sv,
+                                               uint64_t base, const uint64_t* offs) {
+  using R = typename VT::R;
+  using V = typename VT::V;
+  constexpr int L = VT::L;
+  R xs[D][L], ys[D][L], ss[D][L];
+#pragma unroll
+  for (int c = 0; c < D; ++c)
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      VT::get(in[c], l, xs[c][l], ys[c][l]);
+      ss[c][l] = xs[c][l] + ys[c][l];
+    }
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    R P[L], Q[L], S[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) { P[l] = R(0); Q[l] = R(0); S[l] = R(0); }
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const R a = m[r * D + c].x, b = m[r * D + c].y, ab = msum[r * D + c];
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        P[l] = fma(a, xs[c][l], P[l]);
+        Q[l] = fma(b, ys[c][l], Q[l]);
+        S[l] = fma(ab, ss[c][l], S[l]);
+      }
+    }
+    V out;
+#pragma unroll
+    for (int l = 0; l < L; ++l) VT::set(out, l, P[l] - Q[l], S[l] - P[l] - Q[l]);
+    __stcs(sv + base + offs[r], out);
+  }
+}
+
+// same product with the plain 4-multiplication complex MACs
+template <int D, class VT>
+__device__ __forceinline__ void matvec4m_store(const cplx<typename VT::R>* __restrict__ m,
+                                               const typename VT::V (&in)[D], typename VT::V* sv,
+                                               uint64_t base, const uint64_t* offs) {
+  using R = typename VT::R;
+  using V = typename VT::V;
+  constexpr int L = VT::L;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    R accr[L], acci[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) { accr[l] = R(0); acci[l] = R(0); }
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const R mr = m[r * D + c].x, mi = m[r * D + c].y;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        R ar, ai;
+        VT::get(in[c], l, ar, ai);
+        accr[l] = fma(mr, ar, accr[l]);
+        accr[l] = fma(-mi, ai, accr[l]);
+        acci[l] = fma(mr, ai, acci[l]);
+        acci[l] = fma(mi, ar, acci[l]);
+      }
+    }
+    V out;
+#pragma unroll
+    for (int l = 0; l < L; ++l) VT::set(out, l, accr[l], acci[l]);
+    __stcs(sv + base + offs[r], out);
+  }
+}
+
+// DSV_DENSE_4M=1 selects the 4-multiplication products (A/B runs)
+inline bool use_3m() {
+  static const bool v = [] {
+    const char* e = std::getenv("DSV_DENSE_4M");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
 
 // SM count of the current device (cached per device; persistent grids)
 inline int device_sm_count() {

@@ -19,6 +19,7 @@ struct DenseP {
   Geom g;
   uint64_t offs[1 << K];
   cplx<R> m[(1 << K) * (1 << K)];
+  R msum[(1 << K) * (1 << K)];  // re + im of m (3-multiplication products)
 };
 
 template <class VT, int K>
@@ -28,7 +29,7 @@ struct DenseItems {
   static constexpr int value = bytes >= 64 ? 1 : 64 / bytes;
 };
 
-template <int K, class VT, int ITEMS>
+template <int K, class VT, int ITEMS, bool M3>
 __global__ void __launch_bounds__(256)
 k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __restrict__ sv) {
   using V = typename VT::V;
@@ -51,6 +52,10 @@ k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __r
   for (int it = 0; it < ITEMS; ++it) {
     const uint64_t w = w0 + uint64_t(it) * blockDim.x;
     if (w >= p.g.nwork) continue;
+    if constexpr (M3) {  // FMA-bound regime: 3-multiplication complex products
+      matvec3m_store<D, VT>(p.m, p.msum, in[it], sv, base[it], p.offs);
+      continue;
+    }
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       R accr[L], acci[L];
@@ -87,11 +92,17 @@ static cudaError_t dense_reg_t(const Geom& g, const uint64_t* offs, const void* 
   p.g = g;
   for (int j = 0; j < D; ++j) p.offs[j] = offs[j];
   const cplx<R>* m = static_cast<const cplx<R>*>(matrix);
-  for (int i = 0; i < D * D; ++i) p.m[i] = m[i];
+  for (int i = 0; i < D * D; ++i) {
+    p.m[i] = m[i];
+    p.msum[i] = m[i].x + m[i].y;
+  }
   const uint64_t per_block = 256ull * ITEMS;
   const uint64_t blocks = (g.nwork + per_block - 1) / per_block;
   if (blocks == 0) return cudaSuccess;
-  k_dense<K, VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  if (K >= 3 && use_3m())
+    k_dense<K, VT, ITEMS, (K >= 3)><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  else
+    k_dense<K, VT, ITEMS, false><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
   return cudaGetLastError();
 }
 

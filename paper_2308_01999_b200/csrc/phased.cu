@@ -27,6 +27,7 @@ struct PhasedP {
   int chunk_shift[8];      // amp-index shift of each active byte
   uint64_t offs[1 << K];   // member offsets (units)
   cplx<R> m[(1 << K) * (1 << K)];
+  R msum[(1 << K) * (1 << K)];
 };
 
 // sin/cos after explicit reduction to [-pi, pi]: the fast float path is then
@@ -47,7 +48,7 @@ __device__ __forceinline__ void cmul_into(R& xr, R& xi, R er, R ei) {
   xr = r;
 }
 
-template <int K, class VT>
+template <int K, class VT, bool M3>
 __global__ void __launch_bounds__(256)
 k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const typename VT::R* __restrict__ tab,
                typename VT::V* __restrict__ sv) {
@@ -101,30 +102,29 @@ k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const typen
         }
       }
     }
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      R accr[L], acci[L];
-#pragma unroll
-      for (int l = 0; l < L; ++l) { accr[l] = R(0); acci[l] = R(0); }
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        const R mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-          R ar, ai;
-          VT::get(in[c], l, ar, ai);
-          accr[l] = fma(mr, ar, accr[l]);
-          accr[l] = fma(-mi, ai, accr[l]);
-          acci[l] = fma(mr, ai, acci[l]);
-          acci[l] = fma(mi, ar, acci[l]);
-        }
-      }
-      V out;
-#pragma unroll
-      for (int l = 0; l < L; ++l) VT::set(out, l, accr[l], acci[l]);
-      stg_s(sv + base + p.offs[r], out);
-    }
+    if constexpr (M3)
+      matvec3m_store<D, VT>(p.m, p.msum, in, sv, base, p.offs);
+    else
+      matvec4m_store<D, VT>(p.m, in, sv, base, p.offs);
   }
+}
+
+template <int K, class VT, bool M3>
+static cudaError_t phased_go(const PhasedP<K, typename VT::R>& p, size_t smem, uint64_t nwork,
+                             const void* d_tab, void* sv, cudaStream_t st) {
+  using R = typename VT::R;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_dense_phased<K, VT, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_phased<K, VT, M3>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t blocks = (nwork + 255) / 256;
+  const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_phased<K, VT, M3><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const R*>(d_tab),
+                                                                 static_cast<typename VT::V*>(sv));
+  return cudaGetLastError();
 }
 
 template <int K, class VT>
@@ -138,20 +138,13 @@ static cudaError_t phased_t(const PhasedDesc& d, const void* matrix, const void*
   for (int c = 0; c < 8; ++c) p.chunk_shift[c] = c < d.nchunk ? d.chunk_shift[c] : 0;
   for (int j = 0; j < D; ++j) p.offs[j] = d.offs[j];
   const cplx<R>* m = static_cast<const cplx<R>*>(matrix);
-  for (int i = 0; i < D * D; ++i) p.m[i] = m[i];
+  for (int i = 0; i < D * D; ++i) {
+    p.m[i] = m[i];
+    p.msum[i] = m[i].x + m[i].y;
+  }
   const size_t smem = sizeof(R) * size_t(d.nchunk) * 256 * (K + 1);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_dense_phased<K, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_phased<K, VT>, 256, smem);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t blocks = (d.g.nwork + 255) / 256;
-  const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
-  if (blocks > cap) blocks = cap;
-  if (blocks == 0) return cudaSuccess;
-  k_dense_phased<K, VT><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const R*>(d_tab),
-                                                             static_cast<typename VT::V*>(sv));
-  return cudaGetLastError();
+  if (use_3m()) return phased_go<K, VT, true>(p, smem, d.g.nwork, d_tab, sv, st);
+  return phased_go<K, VT, false>(p, smem, d.g.nwork, d_tab, sv, st);
 }
 
 template <class VT>

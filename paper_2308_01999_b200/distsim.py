@@ -28,6 +28,7 @@ from .gates import Gate, PauliString, PermutationGate
 from .plan import (
     TransferStats,
     decompose_swap,
+    localize_phased,
     relabel,
     relocation_pairs,
     segment_selected,
@@ -206,7 +207,24 @@ class SegmentedStateVector:
 
     def apply_gate_distributed(self, g: Gate, upcoming=()) -> None:
         """distsim.py:223-259.  Gate data is cast to the state dtype
-        (StateVector semantics, SURVEY §7.3 hard part 3)."""
+        (StateVector semantics, SURVEY §7.3 hard part 3).  Also accepts the
+        fold fuser's ops (fusion_fold.py): QubitSwap relabels the qubit map,
+        PhasedDenseGate runs per segment with global phase qubits folded in."""
+        from .fusion_fold import PhasedDenseGate, QubitSwap
+
+        if isinstance(g, QubitSwap):
+            self.qubit_map[g.a], self.qubit_map[g.b] = self.qubit_map[g.b], self.qubit_map[g.a]
+            return
+        if isinstance(g, PhasedDenseGate):
+            pairs = self._relocation_pairs([self.qubit_map[q] for q in g.targets], upcoming)
+            if pairs:
+                self.distributed_index_bit_swap(pairs)
+            self._sync_in()
+            for s, st in enumerate(self._devs):
+                m, tb, cross, outside = localize_phased(g, self.qubit_map, self.local_bits, s, self.dtype)
+                st.apply_matrix_phased(m, tb, cross, outside)
+            self._mutated()
+            return
         if len(g.targets) > self.local_bits:
             raise InvalidArgumentError(
                 f"gate arity {len(g.targets)} exceeds local capacity {self.local_bits}"

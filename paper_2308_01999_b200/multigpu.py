@@ -31,7 +31,8 @@ import numpy as np
 
 from .core import InvalidArgumentError, check_swap_pairs
 from .gates import Gate, PauliString, PermutationGate
-from .plan import TransferStats, decompose_swap, relabel, relocation_pairs, segment_selected, split_controls, swap_transfer
+from .plan import (TransferStats, decompose_swap, localize_phased, relabel, relocation_pairs, segment_selected,
+                   split_controls, swap_transfer)
 
 
 class TorchComm:
@@ -104,6 +105,9 @@ class NvlinkSegment:
 
     def apply_genperm(self, perm, diag, bits, ctrls):
         self.seg.apply_genperm(perm, diag, bits, ctrls)
+
+    def apply_matrix_phased(self, m, bits, cross, outside):
+        self.seg.apply_matrix_phased(m, bits, cross, outside)
 
     def swap_bits(self, pairs):
         self.seg.swap_bits(pairs)
@@ -216,11 +220,20 @@ class DistributedStateVector:
 
     # -- gates -------------------------------------------------------------------------------
     def apply(self, g: Gate, upcoming=()) -> None:
+        from .fusion_fold import PhasedDenseGate, QubitSwap
+
+        if isinstance(g, QubitSwap):  # relabel only: no data moves on any rank
+            self.qubit_map[g.a], self.qubit_map[g.b] = self.qubit_map[g.b], self.qubit_map[g.a]
+            return
         if len(g.targets) > self.local_bits:
             raise InvalidArgumentError(f"gate arity {len(g.targets)} exceeds local capacity {self.local_bits}")
         pairs = relocation_pairs(self.qubit_map, self.local_bits, [self.qubit_map[q] for q in g.targets], upcoming)
         if pairs:
             self.distributed_index_bit_swap(pairs)
+        if isinstance(g, PhasedDenseGate):
+            m, tb, cross, outside = localize_phased(g, self.qubit_map, self.local_bits, self.rank, self.dtype)
+            self.seg.apply_matrix_phased(m, tb, cross, outside)
+            return
         tbits = [self.qubit_map[q] for q in g.targets]
         loc, glob = split_controls(self.qubit_map, self.local_bits, g.controls)
         if not segment_selected(self.rank, glob):
@@ -301,14 +314,21 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    ndev = max(1, torch.cuda.device_count())
+    local_dev = local % ndev  # >1 rank per GPU only for functional runs on a 1-GPU box
+    torch.cuda.set_device(local_dev)
+    # NCCL for the scalar reductions; DSV_DIST_BACKEND=gloo allows several ranks per GPU
+    backend = os.environ.get("DSV_DIST_BACKEND", "nccl")
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_dev}"))
+        else:
+            dist.init_process_group(backend)
     comm = TorchComm()
+    comm.local_rank = local_dev
     from . import _native as N
 
-    gates, fc, fuse_s = workload()
-    ops = fc.gates
+    gates, ops, fuse_s = workload(getattr(args, "fusion", "fold"))
     dsv = DistributedStateVector(n_qubits, np.complex64, comm)
     seg = dsv.seg.seg
 
@@ -322,7 +342,7 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
     comm.barrier()
     seg.prof_reset()
     seg.prof_enable(True)
-    clocks = ClockSampler(local).start()
+    clocks = ClockSampler(local_dev).start()
     launches0 = N.launch_count()
     comm.barrier()
     torch.cuda.synchronize()
@@ -354,8 +374,9 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c64",
             "data": "synthetic (QFT-33 circuit generated on the host, state starts at |0>)",
-            "config": {"workload": "qft33_c64_fused_k5_d6", "n_qubits": n_qubits, "circuit_gates": len(gates),
-                       "fused_ops": len(ops), "fusion": list(fusion), "global_bits": dsv.global_bits,
+            "config": {"workload": "qft33_c64_fused_k5", "n_qubits": n_qubits, "circuit_gates": len(gates),
+                       "fused_ops": len(ops), "fusion": getattr(args, "fusion", "fold"),
+                       "global_bits": dsv.global_bits,
                        "l2": "segment >= 8 GiB >> 126 MB L2", "parallelism": f"sv-shard{comm.world} (P2P NVLink swaps)"},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None},

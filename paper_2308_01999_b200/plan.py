@@ -127,7 +127,7 @@ def relocation_pairs(qubit_map: Sequence[int], nloc: int, target_bits: Sequence[
     horizon = len(upcoming) + 1
     next_use: dict[int, int] = {}
     for dist, g in enumerate(upcoming):
-        for q in g.targets:
+        for q in getattr(g, "targets", ()):
             next_use.setdefault(q, dist)
     cands = [b for b in range(nloc) if b not in target_bits]
     if len(need) > len(cands):
@@ -150,3 +150,32 @@ def split_controls(qubit_map: Sequence[int], nloc: int, controls):
 
 def segment_selected(s: int, global_controls) -> bool:
     return all(((s >> b) & 1) == v for b, v in global_controls)
+
+
+def localize_phased(op, qubit_map: Sequence[int], nloc: int, seg: int, dtype):
+    """Per-segment form of a fold-fuser PhasedDenseGate whose targets are
+    local: phase terms on GLOBAL outside qubits are constants inside a segment,
+    so a cross term t x_a x_b (b global) becomes a phase on the target columns
+    with bit a set, and an outside term on a global qubit a scalar phase.
+    Returns (matrix, target_bits, cross[(m, bit, t)], outside[(bit, t)])."""
+    import cmath
+
+    import numpy as np
+
+    m = np.array(op.matrix, dtype=np.complex128, copy=True)
+    pos = {q: i for i, q in enumerate(op.targets)}
+    cols = np.arange(m.shape[1])
+    cross, outside = [], []
+    for a, b, t in op.cross:
+        bit = qubit_map[b]
+        if bit < nloc:
+            cross.append((pos[a], bit, t))
+        elif (seg >> (bit - nloc)) & 1:
+            m[:, ((cols >> pos[a]) & 1) == 1] *= cmath.exp(1j * t)
+    for b, t in op.outside:
+        bit = qubit_map[b]
+        if bit < nloc:
+            outside.append((bit, t))
+        elif (seg >> (bit - nloc)) & 1:
+            m *= cmath.exp(1j * t)
+    return m.astype(dtype), [qubit_map[q] for q in op.targets], cross, outside

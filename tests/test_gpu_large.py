@@ -123,6 +123,18 @@ def test_segmented_equals_single_segment(gbits):
     np.testing.assert_allclose(got, ref, atol=1e-12)
 
 
+def test_segmented_fold_ops_match_single():
+    from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+    n = 16
+    gates = to_gates(gen_qft(n)) + random_gate_sequence(n, 20, np.random.default_rng(9), max_arity=2)
+    ref = run_circuit_sv(gates, n).amplitudes
+    fc = fuse_fold(gates, 4)
+    with SegmentedStateVector(n, 3) as ssv:
+        ssv.run(fc.ops)
+        np.testing.assert_allclose(ssv.to_statevector().amplitudes, ref, atol=1e-12)
+
+
 def test_segmented_expectation_matches_single():
     n = 16
     rng = np.random.default_rng(8)

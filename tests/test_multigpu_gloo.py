@@ -46,6 +46,16 @@ class NumpySegment:
         out[np.asarray(perm)] = np.asarray(diag, self.dtype)[:, None] * self.a[g]
         self.a[g] = out
 
+    def apply_matrix_phased(self, m, bits, cross, outside):
+        idx = np.arange(self.a.size)
+        ph = np.zeros(self.a.size)
+        for mi, b, t in cross:
+            ph += t * (((idx >> bits[mi]) & 1) & ((idx >> b) & 1))
+        for b, t in outside:
+            ph += t * ((idx >> b) & 1)
+        self.a *= np.exp(1j * ph).astype(self.dtype)
+        self.apply_matrix(m, bits, [])
+
     def swap_bits(self, pairs):
         idx = np.arange(self.a.size)
         dst = idx.copy()
@@ -143,8 +153,17 @@ def _worker(rank, world, port, q):
         norm = dsv.norm_squared()
         state = dsv.gather_logical()
         stats = dsv.stats.as_dict()
+        # fold-fuser ops (phased windows with global outside qubits, relabel swaps)
+        from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+        folded = fuse_fold(to_gates(gen_qft(n)), 3)
+        dsv.reset()
+        dsv.run(folded.ops)
+        fstate = dsv.gather_logical()
         if rank == 0:
             want = O.run_circuit(gates, n)
+            fwant = O.run_circuit(to_gates(gen_qft(n)), n)
+            q.put({"fold_err": float(np.abs(fstate - fwant).max())})
             res = {
                 "state_err": float(np.abs(state - want).max()),
                 "prob_err": float(np.abs(probs - O.marginal(want, n, [6, 0, 3])).max()),
@@ -168,10 +187,13 @@ def test_distributed_protocol_over_gloo(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
+    fold = q.get(timeout=240)
+    assert "error" not in fold, fold
     res = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
     assert "error" not in res, res
+    assert fold["fold_err"] < 1e-12
     assert res["state_err"] < 1e-12
     assert res["prob_err"] < 1e-12
     assert res["ev_err"] < 1e-12
