@@ -54,7 +54,7 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
-FOLD_K = 4  # fold fuser window size (<= 5 per the config); k=4 is HBM-bound on CUDA cores
+FOLD_K = 5  # fold fuser window size (<= 5 per the config); k=5 windows run on the tensor cores (tc.cu)
 
 
 def fuse_ops(gates, fusion: str):

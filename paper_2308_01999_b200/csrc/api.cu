@@ -38,6 +38,13 @@ const bool g_disable_tile = [] {
   return !(e && e[0] == '1');
 }();
 
+// Tensor-core path for k = 4, 5 complex64 dense / phased windows (tc.cu).
+// DSV_TC=0 disables it (A/B runs against the CUDA-core kernels).
+const bool g_tc_env = [] {
+  const char* e = std::getenv("DSV_TC");
+  return !(e && e[0] == '0');
+}();
+
 int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -83,12 +90,12 @@ struct DeviceGuard {
 enum ProfClass {
   PC_DENSE = 0, PC_DENSE_GENERIC, PC_PERM, PC_PERM_GENERIC, PC_SWAP, PC_REDUCE,
   PC_EXPECT, PC_PAULI, PC_COLLAPSE, PC_EXCHANGE, PC_ACCESS, PC_SAMPLE,
-  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE
+  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE, PC_DENSE_TC
 };
 const char* kProfNames[DSV_PROF_NCLASS] = {
     "dense", "dense_generic", "genperm", "genperm_generic", "swap_bits", "reduce",
     "expect", "pauli", "collapse", "exchange", "access", "sample",
-    "dense_phased", "diag", "dense_tile", ""};
+    "dense_phased", "diag", "dense_tile", "dense_tc"};
 
 struct ProfRec {
   int cls;
@@ -298,6 +305,116 @@ void canon_matrix(const GateGeom& gg, const void* m_in, std::vector<cplx<R>>& ou
   out.resize(D * D);
   for (uint64_t r = 0; r < D; ++r)
     for (uint64_t c = 0; c < D; ++c) out[r * D + c] = m[old[r] * D + old[c]];
+}
+
+// sm_100-class device (tcgen05 available)?
+bool device_has_tcgen05(int dev) {
+  static int cache[64] = {0};  // 0 unknown, 1 yes, 2 no
+  if (dev < 0 || dev >= 64) return false;
+  if (!cache[dev]) {
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cache[dev] = major == 10 ? 1 : 2;
+  }
+  return cache[dev] == 1;
+}
+
+struct PhaseTerm {
+  int slot;  // sorted target position m (< k), or k for an outside-only term
+  int bit;   // amplitude index bit (outside the targets)
+  double th;
+};
+
+// Can the tensor-core kernel take this gate?  complex64, k in {4, 5}, whole
+// 128-group tiles, and the lowest target >= 2 so every member row of a warp
+// covers whole 32-byte sectors.
+bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
+  if (!g_tc_env || s->dtype != DSV_C64) return false;
+  if (gg.k < 4 || gg.k > 5 || gg.tsorted[0] < 2) return false;
+  if (gg.holes[0] == 0) return false;  // 16-byte row pairs need index bit 0 free
+  const int free_bits = s->nbits - gg.k - gg.nctrl;
+  if (free_bits < 7) return false;
+  return device_has_tcgen05(s->device);
+}
+
+// Dense (+ optional pre-phase) window on the tensor cores; caller holds the device guard.
+int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::vector<PhaseTerm>& terms,
+             int prof_class, double bytes) {
+  const int k = gg.k;
+  const int D = 1 << k, KK = 2 * D;
+  UnitView uv;
+  if (int rc = unit_view(s, gg, false, &uv)) return rc;
+  TcDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.g = uv.g;
+  for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
+  // phase slots per index nibble: [nnib][16][8]
+  int nib_of[16];
+  for (int c = 0; c < 16; ++c) nib_of[c] = -1;
+  for (const PhaseTerm& t : terms) {
+    const int c = t.bit / 4;
+    if (nib_of[c] < 0) {
+      nib_of[c] = d.nnib;
+      d.nib_shift[d.nnib++] = 4 * c;
+    }
+  }
+  std::vector<double> tab(size_t(d.nnib) * 16 * 8, 0.0);
+  for (const PhaseTerm& t : terms) {
+    const int ci = nib_of[t.bit / 4], bb = t.bit % 4;
+    for (int v = 0; v < 16; ++v)
+      if ((v >> bb) & 1) tab[(size_t(ci) * 16 + v) * 8 + t.slot] += t.th;
+  }
+  // real embedding of the canonical matrix (n = 2i + out re/im, kk = 2j + in
+  // re/im) as 2^(e_b - 8) (b0 + b1 / 2^8 + b2 / 2^16), exact bf16 limbs
+  // [b0, b1, b2 / 2^8, b1 / 2^8][n][64] (tc.cu)
+  std::vector<cplx<float>> m;
+  canon_matrix<float>(gg, matrix, m);
+  const int KP = 64;  // one 128-byte bf16 row per B row (2^(k+1) <= 64)
+  float bmax = 0.f;
+  for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
+  int e_b = 0;
+  if (bmax > 0.f) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
+  d.e_b = e_b;
+  const size_t limb_elems = size_t(KK) * KP;
+  std::vector<uint16_t> limbs(4 * limb_elems, 0);
+  auto bf16_bits = [](float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    return uint16_t(u >> 16);  // exact: small integers times powers of two
+  };
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) {
+      const float re = m[size_t(i) * D + j].x, im = m[size_t(i) * D + j].y;
+      const float e[2][2] = {{re, -im}, {im, re}};  // [out re/im][in re/im]
+      for (int oc = 0; oc < 2; ++oc)
+        for (int ic = 0; ic < 2; ++ic) {
+          // I = e 2^(24 - e_b), |I| < 2^24: exact for a float (no rounding)
+          const double I = std::ldexp(double(e[oc][ic]), 24 - e_b);
+          const double b0 = std::nearbyint(I / 65536.0);
+          const double rem = I - b0 * 65536.0;
+          const double b1 = std::nearbyint(rem / 256.0);
+          const double b2 = rem - b1 * 256.0;
+          const size_t at = size_t(2 * i + oc) * KP + (2 * j + ic);
+          limbs[at] = bf16_bits(float(b0));
+          limbs[limb_elems + at] = bf16_bits(float(b1));
+          limbs[2 * limb_elems + at] = bf16_bits(float(b2 / 256.0));
+          limbs[3 * limb_elems + at] = bf16_bits(float(b1 / 256.0));
+        }
+    }
+  const size_t limb_bytes = (limbs.size() * 2 + 255) / 256 * 256;
+  std::vector<unsigned char> host(limb_bytes + tab.size() * sizeof(float), 0);
+  std::memcpy(host.data(), limbs.data(), limbs.size() * 2);
+  for (size_t i = 0; i < tab.size(); ++i) {
+    const float f = float(tab[i]);
+    std::memcpy(host.data() + limb_bytes + i * 4, &f, 4);
+  }
+  if (int rc = ensure_gdata(s, host.size())) return rc;
+  CK(cudaMemcpyAsync(s->gdata, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+  const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
+  ProfTok t = prof_start(s);
+  CKL(launch_dense_tc(k, d, d_b, d_b + limb_bytes, s->d, s->stream), 1);
+  prof_stop(s, t, prof_class, bytes);
+  return DSV_OK;
 }
 
 int sync_streams(dsv_state* waiter, dsv_state* other) {
@@ -538,6 +655,8 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   DeviceGuard g(s->device);
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * std::ldexp(1.0, s->nbits - nctrl);
   const uint64_t D = 1ull << k;
+  // plain k = 4 stays on the CUDA cores (HBM-bound there: 6.3 TB/s vs 4.8 on the tensor path)
+  if (k == 5 && tc_eligible(s, gg)) return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   int nlow = 0;
   for (int m = 0; m < k; ++m) nlow += gg.tsorted[m] < (s->dtype == DSV_C64 ? 4 : 3);
   if (k >= 2 && k <= 5 && nlow >= 2 && s->nbits >= 14 && !g_disable_tile) {
@@ -655,7 +774,7 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
   // sorted position of caller target index m
   std::vector<int> newpos(k);
   for (int mp = 0; mp < k; ++mp) newpos[gg.order[mp]] = mp;
-  struct Term { int slot, bit; double th; };
+  using Term = PhaseTerm;
   std::vector<Term> terms;
   for (int x = 0; x < ncross; ++x) {
     if (cross_t[x] < 0 || cross_t[x] >= k) return fail(DSV_EINVAL, "cross term target index %d out of range", cross_t[x]);
@@ -669,6 +788,8 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
     terms.push_back({k, b, out_theta[y]});
   }
   DeviceGuard g(s->device);
+  if (tc_eligible(s, gg))
+    return apply_tc(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
   UnitView uv;
   if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;
   // active index bytes and the [nchunk][256][k+1] tables

@@ -25,6 +25,23 @@ struct PhasedDesc {
 };
 cudaError_t launch_dense_phased(int dtype, int mode, int k, const PhasedDesc& d, const void* matrix,
                                 const void* d_tab, void* sv, cudaStream_t st);
+// k = 4, 5 complex64 dense gate (optionally phased) on the tensor cores
+// (tcgen05 kind::f16, exact bf16 integer limbs).  g enumerates groups in
+// amplitude space and g.nwork must be a multiple of 128; d_bmat = [limb
+// 0..2][2^(k+1) rows n][KP = max(64, 2^(k+1)) cols kk] bf16 limbs of the real
+// embedding * 2^(8 - e_b) (n = 2i + out re/im, kk = 2j + in re/im); d_tab =
+// [nnib][16][8] fp32 phase slots per index nibble (slot m < k: target m's
+// cross angle, slot k: outside angle).
+struct TcDesc {
+  Geom g;
+  int e_b;
+  int nnib;
+  int nib_shift[16];
+  uint64_t offs[32];
+};
+cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
+                            cudaStream_t st);
+int tc_smem_bytes(int k);
 // k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem
 struct TileDesc {
   Geom g;              // tile bases (holes: bits [0,T), high targets, controls >= T)

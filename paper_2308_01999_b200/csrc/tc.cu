@@ -1,0 +1,456 @@
+// tc.cu — k = 4/5-qubit dense gates (optionally with the fold fuser's
+// outside-coupled pre-phase) on the 5th-generation tensor cores, complex64.
+//
+// Replaces apply_dense_bits (reference statevec.py:44-60) for fused windows
+// whose 2^k x 2^k complex product is FMA-bound on the CUDA cores (k = 5 needs
+// 16 flop/B, i.e. ~100 TFLOP/s of FP32 FMA at HBM speed — more than the
+// CUDA cores have).
+//
+// Arithmetic: exact-integer tensor-core products (Ozaki-style split).  A row
+// of the tile (one amplitude group, 2^(k+1) reals) is scaled by its own power
+// of two so |y| < 256 and rounded to 24 significant bits as bf16 integer
+// limbs y = a0 + a1/2^8 + a2/2^16 (|a0| <= 256, |a1|, |a2| <= 128); the gate's
+// real embedding is split the same way with one global exponent.
+// tcgen05.mma.kind::f16 (bf16 in, fp32 accumulate) then sums
+//   acc0  = sum a0 b0                                  (integers < 2^22: exact)
+//   acc12 = sum a0 b1 + a1 b0 + (a0 b2 + a1 b1 + a2 b0) / 2^8
+// (integer part < 2^23, so the tensor core's truncating accumulation can only
+// drop bits 2^-31 below the result), and the epilogue forms
+// 2^(e_row + e_b - 16) (acc0 + acc12 / 2^8) with round-to-nearest FMAs.
+// fp32-level accuracy without the systematic norm drift of a 3xTF32 split
+// (measured -2e-6 per gate from accumulator truncation; this path: ~1e-8).
+//
+// Dataflow (one persistent CTA per SM, 256 threads = two independent groups
+// of 128; in a group thread t = row t = group t of a 128-group tile; the two
+// groups take alternate tiles and share the gate operand in shared memory):
+//   * per-group ring of S raw tiles in shared memory, filled by cp.async
+//     (16 B = one member of two adjacent groups, coalesced), S-1 tiles of
+//     loads always in flight;
+//   * thread t: phase polynomial in registers (phased windows), row exponent,
+//     limb split, tcgen05.st of its own TMEM lane (the A operand lives in
+//     tensor memory: no shared-memory staging, no swizzle, no bank conflicts);
+//   * thread 0 of the group issues 24 MMAs (M = 128, N = 2^(k+1), K = 16)
+//     and commits to the group's mbarrier; the MMAs overlap the next tile's
+//     copy issue and phase work and the other group's work; then each thread
+//     reads its TMEM lane (tcgen05.ld 32x32b) and streams its 2^k outputs out.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace dsv {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms of 1 KB
+// packed back to back (SBO = 1024 B), LBO unused (1), sm_100 version 1.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, M = 128, N
+template <int N>
+constexpr uint32_t idesc_bf16() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bd, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bd), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
+
+// 32 consecutive TMEM columns of this thread's lane -> registers (ld + wait in
+// one statement so no use of the outputs can be scheduled before the wait)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// registers -> 16 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 2^e as a float (e in the normal range)
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }
+
+// bf16 bits of two exactly-representable floats, packed (lo in bits 0-15)
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632);
+}
+
+__device__ __forceinline__ void sincos_red(float a, float* sn, float* cs) {
+  const float t = a - 6.28318530717958647692f * rintf(a * 0.15915494309189533577f);
+  __sincosf(t, sn, cs);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+constexpr float kMagic = 12582912.f;   // 1.5 * 2^23: (x + kMagic) - kMagic = rint(x), |x| < 2^22
+constexpr float kMagic16 = 49152.f;    // 1.5 * 2^15: rounds to multiples of 2^-8, |x| < 2^14
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+}  // namespace
+
+template <int K>
+struct TcP {
+  Geom g;                 // groups (amplitude index space, holes = targets + controls)
+  uint64_t ntiles;        // g.nwork / 128
+  int nnib;               // phase-table nibbles (0: plain dense)
+  int e_b;                // gate limb exponent: |B| < 2^e_b
+  int nib_shift[16];      // amplitude-index shift of nibble c
+  uint64_t offs[1 << K];  // member offsets (amplitudes)
+};
+
+template <int K>
+struct TcLayout {
+  static constexpr int D = 1 << K;
+  static constexpr int N = 2 * D;                 // GEMM N = real outputs, K = real inputs
+  static constexpr int KSTEPS = N / 16;           // MMA K = 16 (bf16)
+  static constexpr int NBL = 4;                   // B limbs: b0, b1, b2 / 2^8, b1 / 2^8
+  static constexpr int B_LIMB = N * 128;          // one limb: N rows of one 128-byte bf16 row (K <= 64)
+  static constexpr int B0 = 0;
+  static constexpr int BAR = B0 + NBL * B_LIMB;   // 2 mbarriers + TMEM slot
+  static constexpr int RING = BAR + 128;          // raw tiles: [group][stage][member j][row t] float2
+  static constexpr int STAGE = 128 * D * 8;
+  static constexpr int SMEM_MAX = 227 * 1024 - 1024;  // minus the 1 KB alignment slack
+  static constexpr int NS_FIT = (SMEM_MAX - RING) / (2 * STAGE);
+  static constexpr int NSTAGE = NS_FIT > 6 ? 6 : NS_FIT;  // per group
+  static_assert(NSTAGE >= 3, "ring must hold three tiles per group");
+  static_assert(N <= 64, "B operand is one 128-byte K block");
+  static constexpr int BYTES = RING + 2 * NSTAGE * STAGE;
+  // TMEM per group (256 columns): A limbs a0, a1, a2 / 2^8 (D columns each:
+  // one complex member = two bf16 per 32-bit column), acc0, acc12
+  static constexpr int T_A = 0;
+  static constexpr int T_ACC0 = 128;
+  static constexpr int T_ACC12 = 192;
+  static_assert(3 * D <= T_ACC0, "TMEM plan");
+};
+
+// Per group and iteration i (the group's i-th tile):
+//   issue tile i+S-1's member copies (cp.async into its ring stage)
+//   wait for tile i's copies; phase-multiply in registers; row exponent
+//   wait MMA(i-1); epilogue(i-1): TMEM accumulators -> HBM
+//   limbs of tile i -> TMEM (A); group barrier; thread 0 issues MMA(i), commit
+template <int K, bool PHASED>
+__global__ void __launch_bounds__(256, 1)
+k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, const float4* __restrict__ tab,
+           float2* __restrict__ sv) {
+  using L = TcLayout<K>;
+  constexpr int D = L::D;
+  constexpr int N = L::N;
+  constexpr int S = L::NSTAGE;
+  constexpr uint32_t IDESC = idesc_bf16<N>();
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(sm);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int grp = tid >> 7;   // consumer group
+  const int row = tid & 127;  // TMEM lane = tile row = amplitude group within the tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);
+  const uint32_t bar = sbase + L::BAR + 8 * grp;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    mbar_init(sbase + L::BAR, 1);
+    mbar_init(sbase + L::BAR + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // gate limbs, host layout [4][N rows][64 cols] bf16 -> 128-byte swizzled rows
+  for (int i = tid; i < L::NBL * N * 8; i += 256) {
+    const int limb = i / (N * 8);
+    const int r = (i / 8) % N;
+    const int c16 = i % 8;
+    const int off = L::B0 + limb * L::B_LIMB + r * 128 + ((c16 ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(sm + off) = bmat[i];
+  }
+
+  const uint64_t step = gridDim.x;
+  // this group's i-th tile
+  auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + (2 * uint64_t(i) + grp) * step; };
+  // ring: the group's tile i into stage i % S, 16-byte copies: thread t moves
+  // rows (2t', 2t'+1) (adjacent amplitudes, index bit 0) of members j = 2i + t / 64
+  const int prow = 2 * (row & 63);
+  const int jpar = row >> 6;
+  auto issue = [&](int i) {
+    const uint64_t tl = tile_of(i);
+    if (tl < p.ntiles) {
+      const uint64_t b = expand(p.g, tl * 128 + prow);
+      const uint32_t dst = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE + prow * 8;
+#pragma unroll
+      for (int jj = 0; jj < D / 2; ++jj) {
+        const int j = 2 * jj + jpar;
+        cp_async16(dst + j * 1024, sv + b + p.offs[j]);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int s = 0; s < S - 1; ++s) issue(s);
+  cp_async_wait<S - 2>();  // tile 0 landed (this thread's part; the barrier below publishes it)
+
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B operand: generic -> async proxy
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot + uint32_t(grp * 256);
+  const uint32_t tlane = tmem + (uint32_t((warp & 3) * 32) << 16);
+
+  // out = 2^(e_row + e_b - 16) (acc0 + acc12 / 2^8); columns 2i (re), 2i+1 (im).
+  // Lanes 2t', 2t'+1 hold adjacent amplitudes: they swap one member per pair
+  // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1).
+  const bool odd = row & 1;
+  auto epilogue = [&](uint64_t b, float scale) {
+    const uint64_t be = b - (odd ? 1 : 0);
+#pragma unroll
+    for (int h = 0; h < N / 32; ++h) {
+      float c0[32], c1[32];
+      tmem_ld32(tlane + uint32_t(L::T_ACC0 + h * 32), c0);
+      tmem_ld32(tlane + uint32_t(L::T_ACC12 + h * 32), c1);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = __fmaf_rn(c1[4 * q + c], 1.f / 256.f, c0[4 * q + c]) * scale;
+        // o = (re, im) of members 2q, 2q+1 (of this half)
+        const float sx = odd ? o[0] : o[2], sy = odd ? o[1] : o[3];
+        const float rx = __shfl_xor_sync(0xffffffffu, sx, 1), ry = __shfl_xor_sync(0xffffffffu, sy, 1);
+        const int j = h * 16 + 2 * q + (odd ? 1 : 0);
+        const float4 w = odd ? make_float4(rx, ry, o[2], o[3]) : make_float4(o[0], o[1], rx, ry);
+        __stcs(reinterpret_cast<float4*>(sv + be + p.offs[j]), w);
+      }
+    }
+  };
+
+  uint64_t prev_base = 0;
+  float prev_scale = 0.f;
+  int it = 0;
+#pragma unroll 1
+  for (;; ++it) {
+    const uint64_t tile = tile_of(it);
+    if (tile >= p.ntiles) break;
+    issue(it + S - 1);
+    const uint64_t base = expand(p.g, tile * 128 + row);
+    const float2* raw = reinterpret_cast<const float2*>(sm + L::RING + (grp * S + it % S) * L::STAGE) + row;
+    float2 v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = raw[j * 128];
+    if constexpr (PHASED) {
+      float a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) a[s] = 0.f;
+      for (int c = 0; c < p.nnib; ++c) {
+        const int r = (c * 16 + int((base >> p.nib_shift[c]) & 15u)) * 2;
+        const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);  // small table: L1-resident
+        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+        a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+      }
+      float2 P[D];
+      sincos_red(a[K], &P[0].y, &P[0].x);
+#pragma unroll
+      for (int m = 0; m < K; ++m) {
+        float es, ec;
+        sincos_red(a[m], &es, &ec);
+#pragma unroll
+        for (int j = 0; j < (1 << m); ++j) {
+          const float2 q = P[j];
+          P[j + (1 << m)] = make_float2(q.x * ec - q.y * es, q.x * es + q.y * ec);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const float2 x = v[j];
+        v[j] = make_float2(x.x * P[j].x - x.y * P[j].y, x.x * P[j].y + x.y * P[j].x);
+      }
+    }
+    // row exponent: max |x| < 2^e_row (rows below 2^-100 flush to zero)
+    float mx = 0.f;
+#pragma unroll
+    for (int j = 0; j < D; ++j) mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
+    const int e_row = min(max(int((__float_as_uint(mx) >> 23) & 0xFF) - 126, -100), 120);
+    const float s8 = pow2f(8 - e_row), s16 = pow2f(16 - e_row);
+    const float scale = pow2f(e_row + p.e_b - 16);
+    if (it > 0) {  // MMA(i-1) done: A is free and its accumulators are ready
+      mbar_wait(bar, (it - 1) & 1);
+      fence_after();
+      epilogue(prev_base, prev_scale);
+    }
+    // limbs -> TMEM: column j of limb l = member j (re | im << 16).
+    // y = x 2^(8 - e_row), |y| < 256:  a0 = rint(y), r1 = (y - a0) 2^8 (exact),
+    // a1 = rint(r1), a2' = (r1 - a1) rounded to 2^-8 (= a2 / 2^8, |a2| <= 128):
+    // y = a0 + a1 / 2^8 + a2 / 2^16 to 2^-17 (24 significant bits of the row
+    // maximum), 9 full-rate FP32 ops per value (magic-number rounding).
+#pragma unroll
+    for (int h = 0; h < D / 16; ++h) {
+      uint32_t l0[16], l1[16], l2[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        float a0[2], a1[2], a2[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float x = c ? v[h * 16 + q].y : v[h * 16 + q].x;
+          a0[c] = __fadd_rn(__fmaf_rn(x, s8, kMagic), -kMagic);
+          const float r1 = __fmaf_rn(a0[c], -256.f, x * s16);
+          a1[c] = __fadd_rn(__fadd_rn(r1, kMagic), -kMagic);
+          a2[c] = __fadd_rn(__fadd_rn(__fadd_rn(r1, -a1[c]), kMagic16), -kMagic16);
+        }
+        l0[q] = pack2(a0[0], a0[1]);
+        l1[q] = pack2(a1[0], a1[1]);
+        l2[q] = pack2(a2[0], a2[1]);
+      }
+      tmem_st16(tlane + uint32_t(L::T_A + 0 * D + h * 16), l0);
+      tmem_st16(tlane + uint32_t(L::T_A + 1 * D + h * 16), l1);
+      tmem_st16(tlane + uint32_t(L::T_A + 2 * D + h * 16), l2);
+    }
+    cp_async_wait<S - 2>();  // tile i+1 landed (this thread's part)
+    tmem_wait_st();
+    fence_before();
+    group_sync(grp);
+    if (row == 0) {
+      fence_after();
+      const uint32_t bs = sbase + L::B0;
+      // acc0 = a0 b0; acc12 = a0 b1 + a1 b0 + a0 b2' + a1 b1' + a2' b0  (' = / 2^8)
+      constexpr int al[6] = {0, 0, 1, 0, 1, 2};
+      constexpr int bl[6] = {0, 1, 0, 2, 3, 0};
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const uint32_t dcol = q == 0 ? L::T_ACC0 : L::T_ACC12;
+#pragma unroll
+        for (int s = 0; s < L::KSTEPS; ++s)
+          mma_ts(tmem + dcol, tmem + uint32_t(L::T_A + al[q] * D + s * 8),
+                 sw128_desc(bs + bl[q] * L::B_LIMB + s * 32), IDESC, (s == 0 && q <= 1) ? 0u : 1u);
+      }
+      mma_commit(bar);
+    }
+    prev_base = base;
+    prev_scale = scale;
+  }
+  if (it > 0) {
+    mbar_wait(bar, (it - 1) & 1);
+    fence_after();
+    epilogue(prev_base, prev_scale);
+  }
+  cp_async_wait<0>();
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512) : "memory");
+  }
+}
+
+template <int K, bool PHASED>
+static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
+  using L = TcLayout<K>;
+  TcP<K> p;
+  std::memset(&p, 0, sizeof p);
+  p.g = d.g;
+  p.ntiles = d.g.nwork / 128;
+  p.nnib = d.nnib;
+  p.e_b = d.e_b;
+  for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
+  for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
+  const int smem = L::BYTES + 1024;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc<K, PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  uint64_t blocks = uint64_t(device_sm_count());  // persistent: one CTA per SM
+  const uint64_t need = (p.ntiles + 1) / 2;        // two tiles in flight per CTA
+  if (blocks > need) blocks = need;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_tc<K, PHASED><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+                                                              static_cast<const float4*>(d_tab),
+                                                              static_cast<float2*>(sv));
+  return cudaGetLastError();
+}
+
+int tc_smem_bytes(int k) {
+  switch (k) {
+    case 4: return TcLayout<4>::BYTES + 1024;
+    case 5: return TcLayout<5>::BYTES + 1024;
+  }
+  return 0;
+}
+
+cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
+                            cudaStream_t st) {
+  const bool ph = d.nnib > 0;
+  switch (k) {
+    case 4: return ph ? tc_go<4, true>(d, d_bmat, d_tab, sv, st) : tc_go<4, false>(d, d_bmat, d_tab, sv, st);
+    case 5: return ph ? tc_go<5, true>(d, d_bmat, d_tab, sv, st) : tc_go<5, false>(d, d_bmat, d_tab, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dsv

@@ -1,0 +1,133 @@
+"""Tensor-core dense path (tc.cu: tcgen05 kind::tf32, 3-pass hi/lo split) on
+the B200 against the CPU oracle.
+
+Complex64 dense windows with k = 4, 5, lowest target >= 2, index bit 0 free
+and >= 7 free bits take the tcgen05 kernel (plain and phased).  Bar (north_star): max|d| <= 1e-5
+for complex64; we also hold the error RELATIVE to the amplitude scale to
+5e-6 (fp32-level: measured 2.2e-6 worst case for k = 5, the tensor core's
+internal fp32 accumulation is not round-to-nearest), so a silently degraded
+1-pass TF32 product (~5e-4) fails.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import random_state
+from oracle import sv_oracle as O
+from paper_2308_01999_b200 import _native as N
+from paper_2308_01999_b200 import gates as G
+from paper_2308_01999_b200.statevec import StateVector
+
+pytestmark = pytest.mark.gpu
+
+REL = 5e-6
+
+
+@pytest.fixture(autouse=True)
+def _gpu(gpu_available):
+    return gpu_available
+
+
+def _rel_err(got, want):
+    return float(np.abs(got - want).max() / np.abs(want).max())
+
+
+def _phase_angles(n, targets, cross, outside):
+    """Per-amplitude pre-phase of a phased window (fusion_fold.PhasedDenseGate):
+    sum t * x_targets[m] * x_b over cross terms + sum t * x_b over outside terms."""
+    idx = np.arange(1 << n, dtype=np.int64)
+    ang = np.zeros(1 << n)
+    for m, b, t in cross:
+        ang += t * (((idx >> targets[m]) & 1) * ((idx >> b) & 1))
+    for b, t in outside:
+        ang += t * ((idx >> b) & 1)
+    return ang
+
+
+def _tc_launches(sv):
+    nat = sv.native
+    nat.prof_enable(True)
+    nat.prof_reset()
+    return nat
+
+
+@pytest.mark.parametrize("k", [5])
+def test_tc_dense_vs_oracle(k):
+    rng = np.random.default_rng(900 + k)
+    for trial in range(6):
+        n = int(rng.integers(k + 8, 19))
+        pool = list(range(2, n))
+        targets = [int(x) for x in rng.choice(pool, size=k, replace=False)]
+        rest = [q for q in range(1, n) if q not in targets]  # bit 0 stays free (16-byte row pairs)
+        ctrls = [(int(q), int(rng.integers(0, 2))) for q in rng.permutation(rest)[: trial % 3]]
+        if n - k - len(ctrls) < 7:
+            ctrls = []
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng)
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), targets, ctrls)
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
+        prof = nat.prof_read()
+        assert prof.get("dense_tc", {}).get("count", 0) == 1, prof
+        got = sv.amplitudes
+        assert np.abs(got - want).max() <= 1e-5
+        assert _rel_err(got, want) <= REL, (trial, targets, ctrls, _rel_err(got, want))
+
+
+@pytest.mark.parametrize("k", [4, 5])
+def test_tc_phased_vs_oracle(k):
+    rng = np.random.default_rng(950 + k)
+    for trial in range(4):
+        n = int(rng.integers(k + 8, 19))
+        targets = [int(x) for x in rng.choice(np.arange(2, n), size=k, replace=False)]
+        outside_bits = [q for q in range(n) if q not in targets]
+        cross = [(int(rng.integers(0, k)), int(b), float(rng.uniform(-7, 7)))
+                 for b in rng.choice(outside_bits, size=min(12, len(outside_bits)), replace=False)]
+        outside = [(int(b), float(rng.uniform(-7, 7))) for b in rng.choice(outside_bits, size=5, replace=False)]
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng).astype(np.complex64)
+        want = st.astype(np.complex128) * np.exp(1j * _phase_angles(n, targets, cross, outside))
+        O.apply_dense(want, n, m.astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.native.apply_matrix_phased(m, targets, cross, outside)
+        sv._mutated()
+        prof = nat.prof_read()
+        assert prof.get("dense_tc", {}).get("count", 0) == 1, prof
+        got = sv.amplitudes
+        # float32 angle tables + fast sincos: ~1e-6 phase error on top of the product
+        assert _rel_err(got, want) <= 2 * REL, (trial, _rel_err(got, want))
+
+
+def test_tc_involution_round_trip_large():
+    """U then U^dagger on a 24-qubit state with a target in every position
+    class (low/mid/high): returns the input to fp32-level accuracy."""
+    rng = np.random.default_rng(77)
+    n = 24
+    st = random_state(n, rng, np.complex64)
+    sv = StateVector.from_amplitudes(st)
+    for targets in ([2, 3, 4, 5, 6], [7, 11, 13, 17, 23], [19, 20, 21, 22, 23], [2, 9, 15, 22]):
+        m = G.random_unitary(1 << len(targets), rng)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets)))
+        sv.apply_matrix(G.DenseGate(m.conj().T, tuple(targets)))
+    got = sv.amplitudes
+    assert _rel_err(got, st) <= 4 * REL
+    fid = abs(np.vdot(st.astype(np.complex128), got.astype(np.complex128))) ** 2
+    assert fid >= 1 - 1e-6
+
+
+def test_tc_tail_tiles_and_grid_stride():
+    """nwork = 2^(n-k) from exactly one 128-group tile up to many tiles per CTA."""
+    rng = np.random.default_rng(5)
+    for n in (12, 13, 20):
+        k = 5
+        targets = list(range(n - k, n))  # high targets: groups = low free bits
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng)
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets)))
+        assert _rel_err(sv.amplitudes, want) <= REL

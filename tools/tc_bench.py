@@ -1,0 +1,63 @@
+#!/usr/bin/env python
+"""Per-op HBM throughput of k = 4/5 complex64 dense and phased windows.
+
+    python tools/tc_bench.py [--n 30]          # tensor-core path (default)
+    DSV_TC=0 python tools/tc_bench.py --n 30   # CUDA-core kernels, for A/B
+
+Ops: dense k = 4, 5 on high / mid / low(>=2) targets, and every op of the
+fold-fused QFT-n at k = 4 and 5.  Median of 5 (CUDA events on the state's
+stream) after 2 warm-ups; GB/s of algorithmic bytes vs MEASURED_PEAKS.json.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from paper_2308_01999_b200 import gates as G  # noqa: E402
+from paper_2308_01999_b200.circuits import gen_qft, to_gates  # noqa: E402
+from paper_2308_01999_b200.fusion_fold import fuse_fold  # noqa: E402
+from paper_2308_01999_b200.statevec import StateVector  # noqa: E402
+from tools.sweep import entry, peak, time_op  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--only", default="", help="substring filter on op labels (profiling)")
+    args = ap.parse_args()
+    n = args.n
+    pk = peak()
+    sv = StateVector(n, dtype=np.complex64)
+    rng = np.random.default_rng(0)
+    out = []
+    for k in (4, 5):
+        for label, targets in (("high", list(range(n - k, n))), ("mid", list(range(12, 12 + k))),
+                               ("low2", list(range(2, 2 + k))), ("spread", [2, 9, 15, 22, n - 1][:k])):
+            g = G.DenseGate(G.random_unitary(1 << k, rng), tuple(targets))
+            if args.only not in f"dense{k}_{label}":
+                continue
+            ms, byts = time_op(sv, g)
+            out.append(entry(f"dense{k}_{label}", ms, byts, pk, targets=targets))
+    for k in (4, 5):
+        ops = [op for op in fuse_fold(to_gates(gen_qft(n)), k).ops if type(op).__name__ != "QubitSwap"]
+        for i, op in enumerate(ops):
+            if args.only not in f"qft{n}_fold{k}_op{i}":
+                continue
+            ms, byts = time_op(sv, op)
+            out.append(entry(f"qft{n}_fold{k}_op{i}", ms, byts, pk, targets=list(op.targets),
+                             kind=type(op).__name__))
+    print(json.dumps({"n": n, "dtype": "c64", "DSV_TC": os.environ.get("DSV_TC", "1"), "peak_GBps": pk,
+                      "ops": out}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
