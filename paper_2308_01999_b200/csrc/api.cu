@@ -353,10 +353,23 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   for (int c = 0; c < 16; ++c) nib_of[c] = -1;
   for (const PhaseTerm& t : terms) {
     const int c = t.bit / 4;
+    if (c >= 10) return fail(DSV_EUNSUPPORTED, "tensor-core phase table covers index bits < 40");
     if (nib_of[c] < 0) {
       nib_of[c] = d.nnib;
       d.nib_shift[d.nnib++] = 4 * c;
     }
+  }
+  {  // tile rows = the lowest 7 free (non-hole) index bits
+    uint64_t hole_mask = 0, row_mask = 0;
+    for (int b : gg.holes) hole_mask |= 1ull << b;
+    for (int b = 0, got = 0; b < s->nbits && got < 7; ++b)
+      if (!(hole_mask >> b & 1)) {
+        row_mask |= 1ull << b;
+        ++got;
+      }
+    d.coop = 1;
+    for (const PhaseTerm& t : terms)
+      if (row_mask >> t.bit & 1) d.coop = 0;
   }
   std::vector<double> tab(size_t(d.nnib) * 16 * 8, 0.0);
   for (const PhaseTerm& t : terms) {

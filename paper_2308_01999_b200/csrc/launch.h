@@ -35,6 +35,7 @@ cudaError_t launch_dense_phased(int dtype, int mode, int k, const PhasedDesc& d,
 struct TcDesc {
   Geom g;
   int e_b;
+  int coop;  // phase terms avoid the tile's row bits (lowest 7 free bits): one phase vector per tile
   int nnib;
   int nib_shift[16];
   uint64_t offs[32];

@@ -29,7 +29,7 @@
 //   * thread t: phase polynomial in registers (phased windows), row exponent,
 //     limb split, tcgen05.st of its own TMEM lane (the A operand lives in
 //     tensor memory: no shared-memory staging, no swizzle, no bank conflicts);
-//   * thread 0 of the group issues 24 MMAs (M = 128, N = 2^(k+1), K = 16)
+//   * thread 0 of the group issues 20 MMAs (M = 128, N = 2^(k+1..k+2), K = 16)
 //     and commits to the group's mbarrier; the MMAs overlap the next tile's
 //     copy issue and phase work and the other group's work; then each thread
 //     reads its TMEM lane (tcgen05.ld 32x32b) and streams its 2^k outputs out.
@@ -125,6 +125,15 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+// zeros -> 32 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
+  const uint32_t z = 0u;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // 2^e as a float (e in the normal range)
@@ -144,6 +153,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
+constexpr int kTcMaxNib = 10;          // phase-table nibbles: index bits < 40
 constexpr float kMagic = 12582912.f;   // 1.5 * 2^23: (x + kMagic) - kMagic = rint(x), |x| < 2^22
 constexpr float kMagic16 = 49152.f;    // 1.5 * 2^15: rounds to multiples of 2^-8, |x| < 2^14
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -158,6 +168,7 @@ struct TcP {
   uint64_t ntiles;        // g.nwork / 128
   int nnib;               // phase-table nibbles (0: plain dense)
   int e_b;                // gate limb exponent: |B| < 2^e_b
+  int coop;               // phase uniform over a tile's 128 rows: computed once per tile
   int nib_shift[16];      // amplitude-index shift of nibble c
   uint64_t offs[1 << K];  // member offsets (amplitudes)
 };
@@ -171,7 +182,8 @@ struct TcLayout {
   static constexpr int B_LIMB = N * 128;          // one limb: N rows of one 128-byte bf16 row (K <= 64)
   static constexpr int B0 = 0;
   static constexpr int BAR = B0 + NBL * B_LIMB;   // 2 mbarriers + TMEM slot
-  static constexpr int RING = BAR + 128;          // raw tiles: [group][stage][member j][row t] float2
+  static constexpr int PBUF = BAR + 128;          // tile-uniform phases: [group][2][D] float2
+  static constexpr int RING = PBUF + 2 * 2 * D * 8;  // raw tiles: [group][stage][member j][row t] float2
   static constexpr int STAGE = 128 * D * 8;
   static constexpr int SMEM_MAX = 227 * 1024 - 1024;  // minus the 1 KB alignment slack
   static constexpr int NS_FIT = (SMEM_MAX - RING) / (2 * STAGE);
@@ -183,9 +195,35 @@ struct TcLayout {
   // one complex member = two bf16 per 32-bit column), acc0, acc12
   static constexpr int T_A = 0;
   static constexpr int T_ACC0 = 128;
-  static constexpr int T_ACC12 = 192;
-  static_assert(3 * D <= T_ACC0, "TMEM plan");
+  static constexpr int T_ACC12 = T_ACC0 + N;     // adjacent: one N = 2^(k+2) MMA fills both
+  static_assert(3 * D <= T_ACC0 && T_ACC12 + N <= 256, "TMEM plan");
 };
+
+// The group's 20 MMAs for one tile (thread 0 of the group).  TMEM addresses
+// are compile-time constants (the CTA owns all 512 columns, base 0, checked at
+// start).
+//   [acc0 | acc12]  = a0 [b0 | b1]             (one N = 2^(k+2) MMA per K step)
+//   acc12          += a0 b2' + a1 b0 + a1 b1' + a2' b0      (' = / 2^8)
+template <int K, int GRP>
+__device__ __forceinline__ void issue_mma(uint32_t sbase) {
+  using L = TcLayout<K>;
+  constexpr int D = L::D;
+  constexpr int N = L::N;
+  constexpr uint32_t T0 = GRP * 256;
+  constexpr uint32_t ID1 = idesc_bf16<N>(), ID2 = idesc_bf16<2 * N>();
+  const uint32_t bs = sbase + L::B0;
+#pragma unroll
+  for (int s = 0; s < L::KSTEPS; ++s)
+    mma_ts(T0 + L::T_ACC0, T0 + L::T_A + 0 * D + s * 8, sw128_desc(bs + 0 * L::B_LIMB + s * 32), ID2, s > 0);
+  constexpr int al[4] = {0, 1, 1, 2};
+  constexpr int bl[4] = {2, 0, 3, 0};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int s = 0; s < L::KSTEPS; ++s)
+      mma_ts(T0 + L::T_ACC12, T0 + L::T_A + al[q] * D + s * 8, sw128_desc(bs + bl[q] * L::B_LIMB + s * 32), ID1,
+             1u);
+}
 
 // Per group and iteration i (the group's i-th tile):
 //   issue tile i+S-1's member copies (cp.async into its ring stage)
@@ -201,9 +239,12 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   constexpr int N = L::N;
   constexpr int S = L::NSTAGE;
   constexpr uint32_t IDESC = idesc_bf16<N>();
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sbase = smem_u32(sm);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1 KB-aligned base, kept as an offset from smem_raw so the compiler still
+  // sees shared-space accesses (LDS, not generic loads)
+  const uint32_t raw_base = smem_u32(smem_raw);
+  const uint32_t sbase = (raw_base + 1023u) & ~1023u;
+  unsigned char* sm = smem_raw + (sbase - raw_base);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int grp = tid >> 7;   // consumer group
@@ -234,33 +275,75 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   const uint64_t step = gridDim.x;
   // this group's i-th tile
   auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + (2 * uint64_t(i) + grp) * step; };
+  // rows are the lowest 7 free index bits: index(tile, r) = expand(tile * 128) | rowoff(r)
+  const uint64_t e0 = expand(p.g, 0);
+  const uint64_t rowoff = expand(p.g, row) ^ e0;
   // ring: the group's tile i into stage i % S, 16-byte copies: thread t moves
   // rows (2t', 2t'+1) (adjacent amplitudes, index bit 0) of members j = 2i + t / 64
   const int prow = 2 * (row & 63);
   const int jpar = row >> 6;
-  auto issue = [&](int i) {
+  const uint64_t prowoff = expand(p.g, prow) ^ e0;
+  auto issue = [&](int i) -> uint64_t {  // returns the tile's base index
     const uint64_t tl = tile_of(i);
+    uint64_t tb = 0;
     if (tl < p.ntiles) {
-      const uint64_t b = expand(p.g, tl * 128 + prow);
+      tb = expand(p.g, tl * 128);
+      const uint64_t b = tb | prowoff;
       const uint32_t dst = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE + prow * 8;
 #pragma unroll
       for (int jj = 0; jj < D / 2; ++jj) {
-        const int j = 2 * jj + jpar;
-        cp_async16(dst + j * 1024, sv + b + p.offs[j]);
+        const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];  // static indices: no LDC
+        cp_async16(dst + (2 * jj + jpar) * 1024, sv + b + o);
       }
     }
     cp_async_commit();
+    return tb;
   };
-#pragma unroll 1
-  for (int s = 0; s < S - 1; ++s) issue(s);
+  // phase slots of the row at amplitude index `b`: a[m] (target m), a[K] (outside)
+  auto phase_angles = [&](uint64_t b, float (&a)[8]) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) a[s] = 0.f;
+    // small table, L1-resident; unrolled to the maximum nibble count so all
+    // loads issue before the first add
+#pragma unroll
+    for (int c = 0; c < kTcMaxNib; ++c) {
+      if (c < p.nnib) {
+        const int r = (c * 16 + int((b >> p.nib_shift[c]) & 15u)) * 2;
+        const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);
+        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+        a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+      }
+    }
+  };
+  // tile-uniform phases: thread 128 - D + j of the group computes factor j of
+  // the group's tile i (base tb) into buffer i & 1 (published by the next group barrier)
+  float2* Pb = reinterpret_cast<float2*>(sm + L::PBUF) + grp * 2 * D;
+  auto coop_phase = [&](int i, uint64_t tb) {
+    const int j = row - (128 - D);
+    if (PHASED && p.coop && j >= 0 && tile_of(i) < p.ntiles) {
+      float a[8];
+      phase_angles(tb, a);
+      float ang = a[K];
+#pragma unroll
+      for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
+      float sn, cs;
+      sincos_red(ang, &sn, &cs);
+      Pb[(i & 1) * D + j] = make_float2(cs, sn);
+    }
+  };
+  uint64_t tq[S - 1];  // bases of the tiles in flight (static indices only)
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) tq[s] = issue(s);
+  coop_phase(0, tq[0]);
   cp_async_wait<S - 2>();  // tile 0 landed (this thread's part; the barrier below publishes it)
 
+  if (*tmem_slot != 0u) __trap();  // whole-TMEM allocation starts at lane 0, column 0
+  const uint32_t tmem = uint32_t(grp * 256);
+  const uint32_t tlane = tmem + (uint32_t((warp & 3) * 32) << 16);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B operand: generic -> async proxy
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tmem = *tmem_slot + uint32_t(grp * 256);
-  const uint32_t tlane = tmem + (uint32_t((warp & 3) * 32) << 16);
 
   // out = 2^(e_row + e_b - 16) (acc0 + acc12 / 2^8); columns 2i (re), 2i+1 (im).
   // Lanes 2t', 2t'+1 hold adjacent amplitudes: they swap one member per pair
@@ -281,52 +364,58 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
         // o = (re, im) of members 2q, 2q+1 (of this half)
         const float sx = odd ? o[0] : o[2], sy = odd ? o[1] : o[3];
         const float rx = __shfl_xor_sync(0xffffffffu, sx, 1), ry = __shfl_xor_sync(0xffffffffu, sy, 1);
-        const int j = h * 16 + 2 * q + (odd ? 1 : 0);
+        const uint64_t oj = odd ? p.offs[h * 16 + 2 * q + 1] : p.offs[h * 16 + 2 * q];
         const float4 w = odd ? make_float4(rx, ry, o[2], o[3]) : make_float4(o[0], o[1], rx, ry);
-        __stcs(reinterpret_cast<float4*>(sv + be + p.offs[j]), w);
+        __stcs(reinterpret_cast<float4*>(sv + be + oj), w);
       }
     }
   };
 
   uint64_t prev_base = 0;
   float prev_scale = 0.f;
-  int it = 0;
+  int it = 0, stage = 0;
 #pragma unroll 1
   for (;; ++it) {
     const uint64_t tile = tile_of(it);
     if (tile >= p.ntiles) break;
-    issue(it + S - 1);
-    const uint64_t base = expand(p.g, tile * 128 + row);
-    const float2* raw = reinterpret_cast<const float2*>(sm + L::RING + (grp * S + it % S) * L::STAGE) + row;
+    const uint64_t tb_new = issue(it + S - 1);
+    const uint64_t base = tq[0] | rowoff;
+#pragma unroll
+    for (int s = 0; s + 1 < S - 1; ++s) tq[s] = tq[s + 1];
+    tq[S - 2] = tb_new;
+    const float2* raw = reinterpret_cast<const float2*>(sm + L::RING + (grp * S + stage) * L::STAGE) + row;
+    stage = stage + 1 == S ? 0 : stage + 1;
     float2 v[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) v[j] = raw[j * 128];
     if constexpr (PHASED) {
-      float a[8];
+      if (p.coop) {  // the tile's D phase factors, computed last iteration by the last warp
+        const float2* P = Pb + (it & 1) * D;
 #pragma unroll
-      for (int s = 0; s < 8; ++s) a[s] = 0.f;
-      for (int c = 0; c < p.nnib; ++c) {
-        const int r = (c * 16 + int((base >> p.nib_shift[c]) & 15u)) * 2;
-        const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);  // small table: L1-resident
-        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
-        a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
-      }
-      float2 P[D];
-      sincos_red(a[K], &P[0].y, &P[0].x);
-#pragma unroll
-      for (int m = 0; m < K; ++m) {
-        float es, ec;
-        sincos_red(a[m], &es, &ec);
-#pragma unroll
-        for (int j = 0; j < (1 << m); ++j) {
-          const float2 q = P[j];
-          P[j + (1 << m)] = make_float2(q.x * ec - q.y * es, q.x * es + q.y * ec);
+        for (int j = 0; j < D; ++j) {
+          const float2 x = v[j], f = P[j];
+          v[j] = make_float2(x.x * f.x - x.y * f.y, x.x * f.y + x.y * f.x);
         }
-      }
+      } else {
+        float a[8];
+        phase_angles(base, a);
+        float2 P[D];
+        sincos_red(a[K], &P[0].y, &P[0].x);
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const float2 x = v[j];
-        v[j] = make_float2(x.x * P[j].x - x.y * P[j].y, x.x * P[j].y + x.y * P[j].x);
+        for (int m = 0; m < K; ++m) {
+          float es, ec;
+          sincos_red(a[m], &es, &ec);
+#pragma unroll
+          for (int j = 0; j < (1 << m); ++j) {
+            const float2 q = P[j];
+            P[j + (1 << m)] = make_float2(q.x * ec - q.y * es, q.x * es + q.y * ec);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const float2 x = v[j];
+          v[j] = make_float2(x.x * P[j].x - x.y * P[j].y, x.x * P[j].y + x.y * P[j].x);
+        }
       }
     }
     // row exponent: max |x| < 2^e_row (rows below 2^-100 flush to zero)
@@ -368,24 +457,15 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
       tmem_st16(tlane + uint32_t(L::T_A + 1 * D + h * 16), l1);
       tmem_st16(tlane + uint32_t(L::T_A + 2 * D + h * 16), l2);
     }
+    coop_phase(it + 1, tq[0]);
     cp_async_wait<S - 2>();  // tile i+1 landed (this thread's part)
     tmem_wait_st();
     fence_before();
     group_sync(grp);
     if (row == 0) {
       fence_after();
-      const uint32_t bs = sbase + L::B0;
-      // acc0 = a0 b0; acc12 = a0 b1 + a1 b0 + a0 b2' + a1 b1' + a2' b0  (' = / 2^8)
-      constexpr int al[6] = {0, 0, 1, 0, 1, 2};
-      constexpr int bl[6] = {0, 1, 0, 2, 3, 0};
-#pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        const uint32_t dcol = q == 0 ? L::T_ACC0 : L::T_ACC12;
-#pragma unroll
-        for (int s = 0; s < L::KSTEPS; ++s)
-          mma_ts(tmem + dcol, tmem + uint32_t(L::T_A + al[q] * D + s * 8),
-                 sw128_desc(bs + bl[q] * L::B_LIMB + s * 32), IDESC, (s == 0 && q <= 1) ? 0u : 1u);
-      }
+      if (grp == 0) issue_mma<K, 0>(sbase);
+      else issue_mma<K, 1>(sbase);
       mma_commit(bar);
     }
     prev_base = base;
@@ -414,6 +494,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   p.ntiles = d.g.nwork / 128;
   p.nnib = d.nnib;
   p.e_b = d.e_b;
+  p.coop = d.coop;
   for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
   const int smem = L::BYTES + 1024;
