@@ -164,7 +164,7 @@ int dsv_peer_open(int device, int nbits, int dtype, const void* handle64, dsv_st
  * the state's stream and tagged with its kernel class and algorithmic bytes
  * (SURVEY.md section 8(d)).  dsv_prof_read synchronises and aggregates:
  * for class c in [0, DSV_PROF_NCLASS): count[c], ms[c], bytes[c]. */
-#define DSV_PROF_NCLASS 16
+#define DSV_PROF_NCLASS 24
 int dsv_prof_enable(dsv_state* s, int on);
 int dsv_prof_reset(dsv_state* s);
 int dsv_prof_read(dsv_state* s, uint64_t* count, double* ms, double* bytes);

@@ -23,7 +23,7 @@ _lock = threading.Lock()
 
 DSV_OK, DSV_EINVAL, DSV_ECUDA, DSV_ENOMEM, DSV_EUNSUPPORTED = 0, 1, 2, 3, 4
 DSV_C64, DSV_C128 = 0, 1
-PROF_NCLASS = 16
+PROF_NCLASS = 24
 
 _vp = C.c_void_p
 _i32 = C.c_int32

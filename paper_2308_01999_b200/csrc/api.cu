@@ -45,6 +45,13 @@ const bool g_tc_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// Lane-split kernel for k <= 3 complex64 windows on the lowest k bits (low.cu).
+// DSV_LOW=0 disables it.
+const bool g_low_env = [] {
+  const char* e = std::getenv("DSV_LOW");
+  return !(e && e[0] == '0');
+}();
+
 int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -90,12 +97,12 @@ struct DeviceGuard {
 enum ProfClass {
   PC_DENSE = 0, PC_DENSE_GENERIC, PC_PERM, PC_PERM_GENERIC, PC_SWAP, PC_REDUCE,
   PC_EXPECT, PC_PAULI, PC_COLLAPSE, PC_EXCHANGE, PC_ACCESS, PC_SAMPLE,
-  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE, PC_DENSE_TC
+  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE, PC_DENSE_TC, PC_DENSE_LOW
 };
 const char* kProfNames[DSV_PROF_NCLASS] = {
     "dense", "dense_generic", "genperm", "genperm_generic", "swap_bits", "reduce",
     "expect", "pauli", "collapse", "exchange", "access", "sample",
-    "dense_phased", "diag", "dense_tile", "dense_tc"};
+    "dense_phased", "diag", "dense_tile", "dense_tc", "dense_low"};
 
 struct ProfRec {
   int cls;
@@ -430,6 +437,52 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   return DSV_OK;
 }
 
+// complex64, 1 <= k <= 3, targets exactly bits 0..k-1, whole warps of lanes
+bool low_eligible(const dsv_state* s, const GateGeom& gg) {
+  if (!g_low_env || s->dtype != DSV_C64 || gg.k < 1 || gg.k > 3) return false;
+  for (int m = 0; m < gg.k; ++m)
+    if (gg.tsorted[m] != m) return false;
+  // lane-items (groups x 2^(k-1)) fill whole 1024-item passes: no tail guards
+  const int L = 1 << (gg.k - 1);
+  const int free_bits = s->nbits - gg.k - gg.nctrl;
+  return free_bits >= 0 && (std::ldexp(1.0, free_bits) * L) >= 1024.0;
+}
+
+// Low-target window (+ optional pre-phase); caller holds the device guard.
+int apply_low(dsv_state* s, const GateGeom& gg, const void* matrix, const std::vector<PhaseTerm>& terms,
+              int prof_class, double bytes) {
+  const int k = gg.k;
+  UnitView uv;
+  if (int rc = unit_view(s, gg, false, &uv)) return rc;
+  LowDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.g = uv.g;
+  d.plain = gg.nctrl == 0;
+  // phase slots by index byte: [8][256][4] (bytes without terms stay zero)
+  uint32_t used = 0;
+  for (const PhaseTerm& t : terms) used |= 1u << (t.bit / 8);
+  for (int c = 0; c < 8; ++c)
+    if (used >> c & 1) d.chunk_shift[d.nchunk++] = 8 * c;
+  if (!terms.empty()) {
+    std::vector<double> tab(size_t(8) * 256 * 4, 0.0);
+    for (const PhaseTerm& t : terms) {
+      const int c = t.bit / 8, bb = t.bit % 8;
+      for (int v = 0; v < 256; ++v)
+        if ((v >> bb) & 1) tab[(size_t(c) * 256 + v) * 4 + t.slot] += t.th;
+    }
+    std::vector<float> host(tab.size());
+    for (size_t i = 0; i < tab.size(); ++i) host[i] = float(tab[i]);
+    if (int rc = ensure_gdata(s, host.size() * sizeof(float))) return rc;
+    CK(cudaMemcpyAsync(s->gdata, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  }
+  std::vector<cplx<float>> m;
+  canon_matrix<float>(gg, matrix, m);
+  ProfTok t = prof_start(s);
+  CKL(launch_dense_low(k, d, m.data(), s->gdata, s->d, s->stream), 1);
+  prof_stop(s, t, prof_class, bytes);
+  return DSV_OK;
+}
+
 int sync_streams(dsv_state* waiter, dsv_state* other) {
   if (waiter->stream == other->stream) return DSV_OK;
   cudaEvent_t e;
@@ -670,6 +723,7 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   const uint64_t D = 1ull << k;
   // plain k = 4 stays on the CUDA cores (HBM-bound there: 6.3 TB/s vs 4.8 on the tensor path)
   if (k == 5 && tc_eligible(s, gg)) return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
+  if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
   int nlow = 0;
   for (int m = 0; m < k; ++m) nlow += gg.tsorted[m] < (s->dtype == DSV_C64 ? 4 : 3);
   if (k >= 2 && k <= 5 && nlow >= 2 && s->nbits >= 14 && !g_disable_tile) {
@@ -803,6 +857,8 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
   DeviceGuard g(s->device);
   if (tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  if (low_eligible(s, gg))
+    return apply_low(s, gg, matrix, terms, PC_DENSE_LOW, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
   UnitView uv;
   if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;
   // active index bytes and the [nchunk][256][k+1] tables

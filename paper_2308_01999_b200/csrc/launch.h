@@ -43,6 +43,19 @@ struct TcDesc {
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);
 int tc_smem_bytes(int k);
+// k = 1..3 complex64 gate (optionally phased) whose targets are exactly the
+// lowest k bits: 2^(k-1) lanes per group, one float4 each.  g enumerates
+// groups (holes = targets + controls), g.nwork * 2^(k-1) a multiple of 32;
+// d_tab = [nchunk][256][4] fp32 phase slots per index byte (slot m < k:
+// target m's cross angle, slot k: outside angle).
+struct LowDesc {
+  Geom g;
+  int plain;  // no controls: group w starts at w << k
+  int nchunk;
+  int chunk_shift[8];
+};
+cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const void* d_tab, void* sv,
+                             cudaStream_t st);
 // k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem
 struct TileDesc {
   Geom g;              // tile bases (holes: bits [0,T), high targets, controls >= T)

@@ -1,0 +1,173 @@
+// low.cu — complex64 dense k-qubit gates (k = 1..3) whose targets are exactly
+// the LOWEST k index bits, optionally preceded by the fold fuser's
+// outside-coupled phase polynomial (the last window of a folded QFT, e.g.
+// QFT-33 at k = 5 ends on qubits (0, 1, 2)).  Replaces apply_dense_bits
+// (reference statevec.py:44-60) for that layout.
+//
+// A group (2^k consecutive amplitudes, 2^(k+3) bytes) is spread over
+// L = 2^(k-1) lanes, one 16-byte float4 (two members) each, so every warp
+// load/store is a fully coalesced 512-byte run — the register path's
+// one-thread-per-group layout strides 64 bytes between lanes here.  Each lane
+// applies the phase to its own two members (one sincos each: the member's
+// angle is the outside angle plus the cross angles of its set target bits),
+// gathers the group with L-1 float4 shuffles and computes its two output rows
+// from matrix rows held in registers for the whole persistent loop.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace dsv {
+
+constexpr int kLowItems = 4;
+
+template <int K>
+struct LowP {
+  Geom g;                 // groups: holes = targets (bits 0..k-1) + controls
+  int nchunk;             // phase-table index bytes in use (0: plain dense)
+  int plain;              // no controls: group w starts at amplitude w << k
+  uint32_t used;          // bit c: index byte c carries phase terms (table row block c)
+  cplx<float> m[(1 << K) * (1 << K)];
+};
+
+__device__ __forceinline__ void sincos_low(float a, float* sn, float* cs) {
+  const float t = a - 6.28318530717958647692f * rintf(a * 0.15915494309189533577f);
+  __sincosf(t, sn, cs);
+}
+
+template <int K, bool PHASED>
+__global__ void __launch_bounds__(256)
+k_dense_low(const __grid_constant__ LowP<K> p, const float4* __restrict__ tab, float4* __restrict__ sv4) {
+  constexpr int D = 1 << K;
+  constexpr int L = D / 2;  // lanes per group
+  extern __shared__ float4 stab[];  // [index byte 0..7][256] phase slots (target m: slot m, outside: slot K)
+  if constexpr (PHASED) {
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) stab[i] = tab[i];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (L - 1);
+  const int gl0 = lane & ~(L - 1);
+  // this lane's two output rows, 2 sub and 2 sub + 1, kept in registers
+  float mr[2][D][2];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const cplx<float> z = p.m[(2 * sub + rr) * D + c];
+      mr[rr][c][0] = z.x;
+      mr[rr][c][1] = z.y;
+    }
+  // U lane-items per thread per pass, all loads first (memory-level parallelism);
+  // the host guarantees nwork * L is a multiple of 256 U: no per-item guards,
+  // so the shuffles stay convergent
+  constexpr int U = kLowItems;
+  const uint64_t npass = p.g.nwork * L / (256 * U);
+  // block-uniform trip count: the compiler sees convergent shuffles
+  for (uint64_t pass = blockIdx.x; pass < npass; pass += gridDim.x) {
+    const uint64_t t0 = pass * (256 * U) + threadIdx.x;
+    uint64_t base[U];
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t t = t0 + uint64_t(u) * 256;
+      base[u] = p.plain ? (t / L) << K : expand(p.g, t / L);  // multiple of 2^k
+      v[u] = __ldcs(sv4 + (base[u] >> 1) + sub);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if constexpr (PHASED) {
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if ((p.used >> c) & 1u) {  // compile-time byte position: cheap extraction
+            const float4 x = stab[c * 256 + int((base[u] >> (8 * c)) & 255u)];
+            a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+          }
+        }
+        float ang[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = 2 * sub + h;
+          ang[h] = a[K];
+#pragma unroll
+          for (int m = 0; m < K; ++m) ang[h] += ((j >> m) & 1) ? a[m] : 0.f;
+        }
+        float s0, c0, s1, c1;
+        sincos_low(ang[0], &s0, &c0);
+        sincos_low(ang[1], &s1, &c1);
+        const float4 x = v[u];
+        v[u] = make_float4(x.x * c0 - x.y * s0, x.x * s0 + x.y * c0, x.z * c1 - x.w * s1, x.z * s1 + x.w * c1);
+      }
+      float in[D][2];
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        float4 w;
+        if constexpr (L == 1) {
+          w = v[u];
+        } else {
+          w.x = __shfl_sync(0xffffffffu, v[u].x, gl0 + i);
+          w.y = __shfl_sync(0xffffffffu, v[u].y, gl0 + i);
+          w.z = __shfl_sync(0xffffffffu, v[u].z, gl0 + i);
+          w.w = __shfl_sync(0xffffffffu, v[u].w, gl0 + i);
+        }
+        in[2 * i][0] = w.x;
+        in[2 * i][1] = w.y;
+        in[2 * i + 1][0] = w.z;
+        in[2 * i + 1][1] = w.w;
+      }
+      float o[2][2];
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        float re = 0.f, im = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          re = fmaf(mr[rr][c][0], in[c][0], re);
+          re = fmaf(-mr[rr][c][1], in[c][1], re);
+          im = fmaf(mr[rr][c][0], in[c][1], im);
+          im = fmaf(mr[rr][c][1], in[c][0], im);
+        }
+        o[rr][0] = re;
+        o[rr][1] = im;
+      }
+      __stcs(sv4 + (base[u] >> 1) + sub, make_float4(o[0][0], o[0][1], o[1][0], o[1][1]));
+    }
+  }
+}
+
+template <int K, bool PHASED>
+static cudaError_t low_go(const LowDesc& d, const void* matrix, const void* d_tab, void* sv, cudaStream_t st) {
+  LowP<K> p;
+  std::memset(&p, 0, sizeof p);
+  p.g = d.g;
+  p.nchunk = d.nchunk;
+  p.plain = d.plain;
+  for (int c = 0; c < d.nchunk; ++c) p.used |= 1u << (d.chunk_shift[c] / 8);
+  std::memcpy(p.m, matrix, sizeof(p.m));
+  const int smem = PHASED ? 8 * 256 * 16 : 0;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_low<K, PHASED>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  constexpr int L = (1 << K) / 2;
+  uint64_t blocks = (d.g.nwork * L + 256 * kLowItems - 1) / (256 * kLowItems);
+  const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_low<K, PHASED><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const float4*>(d_tab),
+                                                             static_cast<float4*>(sv));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const void* d_tab, void* sv,
+                             cudaStream_t st) {
+  const bool ph = d.nchunk > 0;
+  switch (k) {
+    case 1: return ph ? low_go<1, true>(d, matrix, d_tab, sv, st) : low_go<1, false>(d, matrix, d_tab, sv, st);
+    case 2: return ph ? low_go<2, true>(d, matrix, d_tab, sv, st) : low_go<2, false>(d, matrix, d_tab, sv, st);
+    case 3: return ph ? low_go<3, true>(d, matrix, d_tab, sv, st) : low_go<3, false>(d, matrix, d_tab, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dsv

@@ -131,3 +131,46 @@ def test_tc_tail_tiles_and_grid_stride():
         sv = StateVector.from_amplitudes(st)
         sv.apply_matrix(G.DenseGate(m, tuple(targets)))
         assert _rel_err(sv.amplitudes, want) <= REL
+
+
+# ---- lane-split kernel: k <= 3 windows on the lowest k bits (low.cu) ------------------------
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_low_dense_vs_oracle(k):
+    rng = np.random.default_rng(700 + k)
+    for trial in range(4):
+        n = int(rng.integers(14, 19))  # >= 1024 lane-items: whole passes
+        targets = [int(x) for x in rng.permutation(k)]  # bits 0..k-1, any order
+        rest = list(range(k, n))
+        ctrls = [(int(q), int(rng.integers(0, 2))) for q in rng.permutation(rest)[: trial % 3]]
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng)
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), targets, ctrls)
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
+        assert nat.prof_read().get("dense_low", {}).get("count", 0) == 1
+        assert _rel_err(sv.amplitudes, want) <= 1e-6
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_low_phased_vs_oracle(k):
+    rng = np.random.default_rng(750 + k)
+    for trial in range(3):
+        n = int(rng.integers(12, 19))
+        targets = list(range(k))
+        outside_bits = list(range(k, n))
+        cross = [(int(rng.integers(0, k)), int(b), float(rng.uniform(-7, 7)))
+                 for b in rng.choice(outside_bits, size=min(14, len(outside_bits)), replace=False)]
+        outside = [(int(b), float(rng.uniform(-7, 7))) for b in rng.choice(outside_bits, size=4, replace=False)]
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng).astype(np.complex64)
+        want = st.astype(np.complex128) * np.exp(1j * _phase_angles(n, targets, cross, outside))
+        O.apply_dense(want, n, m.astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.native.apply_matrix_phased(m, targets, cross, outside)
+        sv._mutated()
+        assert nat.prof_read().get("dense_low", {}).get("count", 0) == 1
+        assert _rel_err(sv.amplitudes, want) <= 2 * REL, (trial, _rel_err(sv.amplitudes, want))
