@@ -65,23 +65,38 @@ k_dense_low(const __grid_constant__ LowP<K> p, const float4* __restrict__ tab, f
   constexpr int U = kLowItems;
   const uint64_t npass = p.g.nwork * L / (256 * U);
   // block-uniform trip count: the compiler sees convergent shuffles
+  const int warp = threadIdx.x >> 5;
   for (uint64_t pass = blockIdx.x; pass < npass; pass += gridDim.x) {
-    const uint64_t t0 = pass * (256 * U) + threadIdx.x;
+    // a warp's U x 32 lane-items = 256 consecutive amplitudes (256-aligned):
+    // without controls, index bytes 1..7 are uniform over the warp's items
+    const uint64_t t0 = pass * (256 * U) + warp * (32 * U) + lane;
     uint64_t base[U];
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t t = t0 + uint64_t(u) * 256;
+      const uint64_t t = t0 + uint64_t(u) * 32;
       base[u] = p.plain ? (t / L) << K : expand(p.g, t / L);  // multiple of 2^k
       v[u] = __ldcs(sv4 + (base[u] >> 1) + sub);
+    }
+    float4 hi = make_float4(0.f, 0.f, 0.f, 0.f);  // phase slots from index bytes 1..7
+    if constexpr (PHASED) {
+      if (p.plain) {
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+          if ((p.used >> c) & 1u) {  // warp-uniform row: broadcast
+            const float4 x = stab[c * 256 + int((base[0] >> (8 * c)) & 255u)];
+            hi.x += x.x; hi.y += x.y; hi.z += x.z; hi.w += x.w;
+          }
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if constexpr (PHASED) {
-        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        float a[4] = {hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          if ((p.used >> c) & 1u) {  // compile-time byte position: cheap extraction
+          if ((p.used >> c) & 1u && (c == 0 || !p.plain)) {  // compile-time byte position
             const float4 x = stab[c * 256 + int((base[u] >> (8 * c)) & 255u)];
             a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
           }
