@@ -333,12 +333,14 @@ struct PhaseTerm {
 };
 
 // Can the tensor-core kernel take this gate?  complex64, k in {4, 5}, whole
-// 128-group tiles, and the lowest target >= 2 so every member row of a warp
-// covers whole 32-byte sectors.
+// 128-group tiles.  Index bit 0 free selects 16-byte row-pair copies (PAIR),
+// else each thread moves its own row 8 bytes per member.
 bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
   if (!g_tc_env || s->dtype != DSV_C64) return false;
-  if (gg.k < 4 || gg.k > 5 || gg.tsorted[0] < 2) return false;
-  if (gg.holes[0] == 0) return false;  // 16-byte row pairs need index bit 0 free
+  if (gg.k < 4 || gg.k > 5) return false;
+  // rows are the lowest free bits: with bits 0 and 1 both holes, consecutive
+  // rows sit >= 32 bytes apart and the per-row 8-byte copies waste sectors
+  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1) return false;
   const int free_bits = s->nbits - gg.k - gg.nctrl;
   if (free_bits < 7) return false;
   return device_has_tcgen05(s->device);
@@ -354,6 +356,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   TcDesc d;
   std::memset(&d, 0, sizeof d);
   d.g = uv.g;
+  d.pair = gg.holes[0] != 0;
   for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
   // phase slots per index nibble: [nnib][16][8]
   int nib_of[16];

@@ -36,6 +36,7 @@ struct TcDesc {
   Geom g;
   int e_b;
   int coop;  // phase terms avoid the tile's row bits (lowest 7 free bits): one phase vector per tile
+  int pair;  // index bit 0 free: 16-byte copies/stores of adjacent row pairs (else 8 B per row)
   int nnib;
   int nib_shift[16];
   uint64_t offs[32];

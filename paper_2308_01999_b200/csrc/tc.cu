@@ -149,6 +149,9 @@ __device__ __forceinline__ void sincos_red(float a, float* sn, float* cs) {
   __sincosf(t, sn, cs);
 }
 
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -230,7 +233,7 @@ __device__ __forceinline__ void issue_mma(uint32_t sbase) {
 //   wait for tile i's copies; phase-multiply in registers; row exponent
 //   wait MMA(i-1); epilogue(i-1): TMEM accumulators -> HBM
 //   limbs of tile i -> TMEM (A); group barrier; thread 0 issues MMA(i), commit
-template <int K, bool PHASED>
+template <int K, bool PHASED, bool PAIR>
 __global__ void __launch_bounds__(256, 1)
 k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, const float4* __restrict__ tab,
            float2* __restrict__ sv) {
@@ -288,12 +291,19 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
     uint64_t tb = 0;
     if (tl < p.ntiles) {
       tb = expand(p.g, tl * 128);
-      const uint64_t b = tb | prowoff;
-      const uint32_t dst = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE + prow * 8;
+      if constexpr (PAIR) {
+        const uint64_t b = tb | prowoff;
+        const uint32_t dst = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE + prow * 8;
 #pragma unroll
-      for (int jj = 0; jj < D / 2; ++jj) {
-        const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];  // static indices: no LDC
-        cp_async16(dst + (2 * jj + jpar) * 1024, sv + b + o);
+        for (int jj = 0; jj < D / 2; ++jj) {
+          const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];  // static indices: no LDC
+          cp_async16(dst + (2 * jj + jpar) * 1024, sv + b + o);
+        }
+      } else {  // index bit 0 is a target or control: each thread copies its own row, 8 B per member
+        const uint64_t b = tb | rowoff;
+        const uint32_t dst = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE + row * 8;
+#pragma unroll
+        for (int j = 0; j < D; ++j) cp_async8(dst + j * 1024, sv + b + p.offs[j]);
       }
     }
     cp_async_commit();
@@ -350,6 +360,21 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1).
   const bool odd = row & 1;
   auto epilogue = [&](uint64_t b, float scale) {
+    if constexpr (!PAIR) {  // 8-byte stores of this row's members
+#pragma unroll
+      for (int h = 0; h < N / 32; ++h) {
+        float c0[32], c1[32];
+        tmem_ld32(tlane + uint32_t(L::T_ACC0 + h * 32), c0);
+        tmem_ld32(tlane + uint32_t(L::T_ACC12 + h * 32), c1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float re = __fmaf_rn(c1[2 * i], 1.f / 256.f, c0[2 * i]) * scale;
+          const float im = __fmaf_rn(c1[2 * i + 1], 1.f / 256.f, c0[2 * i + 1]) * scale;
+          __stcs(sv + b + p.offs[h * 16 + i], make_float2(re, im));
+        }
+      }
+      return;
+    }
     const uint64_t be = b - (odd ? 1 : 0);
 #pragma unroll
     for (int h = 0; h < N / 32; ++h) {
@@ -485,7 +510,7 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   }
 }
 
-template <int K, bool PHASED>
+template <int K, bool PHASED, bool PAIR>
 static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
   using L = TcLayout<K>;
   TcP<K> p;
@@ -502,7 +527,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_tc<K, PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc<K, PHASED, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -510,7 +535,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   const uint64_t need = (p.ntiles + 1) / 2;        // two tiles in flight per CTA
   if (blocks > need) blocks = need;
   if (blocks == 0) return cudaSuccess;
-  k_dense_tc<K, PHASED><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+  k_dense_tc<K, PHASED, PAIR><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
                                                               static_cast<const float4*>(d_tab),
                                                               static_cast<float2*>(sv));
   return cudaGetLastError();
@@ -524,12 +549,18 @@ int tc_smem_bytes(int k) {
   return 0;
 }
 
+template <int K>
+static cudaError_t tc_k(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
+  const bool ph = d.nnib > 0;
+  if (d.pair) return ph ? tc_go<K, true, true>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, true>(d, d_bmat, d_tab, sv, st);
+  return ph ? tc_go<K, true, false>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, false>(d, d_bmat, d_tab, sv, st);
+}
+
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st) {
-  const bool ph = d.nnib > 0;
   switch (k) {
-    case 4: return ph ? tc_go<4, true>(d, d_bmat, d_tab, sv, st) : tc_go<4, false>(d, d_bmat, d_tab, sv, st);
-    case 5: return ph ? tc_go<5, true>(d, d_bmat, d_tab, sv, st) : tc_go<5, false>(d, d_bmat, d_tab, sv, st);
+    case 4: return tc_k<4>(d, d_bmat, d_tab, sv, st);
+    case 5: return tc_k<5>(d, d_bmat, d_tab, sv, st);
   }
   return cudaErrorInvalidValue;
 }

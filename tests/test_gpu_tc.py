@@ -76,12 +76,36 @@ def test_tc_dense_vs_oracle(k):
         assert _rel_err(got, want) <= REL, (trial, targets, ctrls, _rel_err(got, want))
 
 
+@pytest.mark.parametrize("case", ["bit1", "ctrl0", "spread0"])
+def test_tc_dense_low_bits_vs_oracle(case):
+    """Index bit 0 a target or control: the 8-byte-per-row (non-pair) copies."""
+    rng = np.random.default_rng(hash(case) % 1000)
+    n = 16
+    targets, ctrls = {
+        "bit1": ([1, 2, 3, 9, 14], []),
+        "ctrl0": ([2, 5, 8, 11, 15], [(0, 1)]),
+        "spread0": ([0, 4, 7, 10, 13], [(15, 0)]),
+    }[case]
+    targets = [int(t) for t in rng.permutation(targets)]
+    st = random_state(n, rng, np.complex64)
+    m = G.random_unitary(32, rng)
+    want = st.astype(np.complex128)
+    O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), targets, ctrls)
+    sv = StateVector.from_amplitudes(st)
+    nat = _tc_launches(sv)
+    sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
+    assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1
+    assert _rel_err(sv.amplitudes, want) <= REL
+
+
 @pytest.mark.parametrize("k", [4, 5])
 def test_tc_phased_vs_oracle(k):
     rng = np.random.default_rng(950 + k)
     for trial in range(4):
         n = int(rng.integers(k + 8, 19))
         targets = [int(x) for x in rng.choice(np.arange(2, n), size=k, replace=False)]
+        if trial == 3:
+            targets[0] = 0  # index bit 0 a target: per-row copies
         outside_bits = [q for q in range(n) if q not in targets]
         cross = [(int(rng.integers(0, k)), int(b), float(rng.uniform(-7, 7)))
                  for b in rng.choice(outside_bits, size=min(12, len(outside_bits)), replace=False)]

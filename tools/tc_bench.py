@@ -62,7 +62,8 @@ def main():
     out = []
     for k in (4, 5):
         for label, targets in (("high", list(range(n - k, n))), ("mid", list(range(12, 12 + k))),
-                               ("low2", list(range(2, 2 + k))), ("spread", [2, 9, 15, 22, n - 1][:k])):
+                               ("low2", list(range(2, 2 + k))), ("spread", [2, 9, 15, 22, n - 1][:k]),
+                               ("low0", list(range(k))), ("with0", [0, 7, 13, 20, 25][:k])):
             g = G.DenseGate(G.random_unitary(1 << k, rng), tuple(targets))
             if args.only not in f"dense{k}_{label}":
                 continue
