@@ -60,6 +60,11 @@ int dsv_launch_count(uint64_t* out);
 
 /* ---- lifecycle (statevec.py:122-128 StateVector.__init__, distsim.py:70-84) */
 /* Allocate 2^nbits amplitudes on `device`, initialised to |0...0>. */
+/* Destroyed states park their device buffer in a small per-process cache that
+ * dsv_state_create reuses for the same (device, size); a failed allocation
+ * empties it first.  This releases the cache (device < 0: all devices).
+ * DSV_POOL=0 in the environment disables caching. */
+int dsv_pool_release(int device);
 int dsv_state_create(int device, int nbits, int dtype, dsv_state** out);
 int dsv_state_destroy(dsv_state* s);
 int dsv_state_info(const dsv_state* s, int* device, int* nbits, int* dtype);

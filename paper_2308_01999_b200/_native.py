@@ -42,6 +42,7 @@ SIGNATURES: dict[str, list] = {
     "dsv_device_count": [C.POINTER(_int)],
     "dsv_launch_count": [_u64p],
     "dsv_state_create": [_int, _int, _int, C.POINTER(_vp)],
+    "dsv_pool_release": [_int],
     "dsv_state_destroy": [_vp],
     "dsv_state_info": [_vp, C.POINTER(_int), C.POINTER(_int), C.POINTER(_int)],
     "dsv_state_device_ptr": [_vp, C.POINTER(_vp)],
@@ -155,6 +156,11 @@ def device_count() -> int:
     n = C.c_int(0)
     rc = lib().dsv_device_count(C.byref(n))
     return n.value if rc == DSV_OK else 0
+
+
+def pool_release(device: int = -1) -> None:
+    """Free the cached state buffers (device < 0: every device)."""
+    call("dsv_pool_release", int(device))
 
 
 def launch_count() -> int:

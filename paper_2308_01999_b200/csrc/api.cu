@@ -119,6 +119,7 @@ struct dsv_state {
   void* d = nullptr;
   bool owned = true;
   bool ipc = false;
+  bool exported = false;  // an IPC handle was handed out: never recycle the allocation
   cudaStream_t stream = nullptr;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -583,6 +584,79 @@ int dsv_launch_count(uint64_t* out) {
   return DSV_OK;
 }
 
+// ---- state-buffer cache ------------------------------------------------------------
+// cudaMalloc / cudaFree of a 64 GiB state cost tens to hundreds of ms (measured
+// 23-56 ms / 145-837 ms at n = 33), paid per circuit by every user who builds a
+// fresh StateVector.  Destroyed states park their buffer here (exact size and
+// device match on reuse); an allocation that fails for lack of memory first
+// releases the cache.  DSV_POOL=0 disables it; dsv_pool_release() empties it.
+namespace {
+struct PoolEntry {
+  int device;
+  size_t bytes;
+  void* ptr;
+  // the state's private stream and scratch buffers ride along (cudaFree and
+  // cudaStreamDestroy synchronise the device: ~15 ms per state otherwise)
+  cudaStream_t stream;
+  void* scratch;
+  size_t scratch_bytes;
+  void* gdata;
+  size_t gdata_bytes;
+};
+std::mutex g_pool_mu;
+std::vector<PoolEntry> g_pool;
+constexpr size_t kPoolMaxEntries = 4;
+const bool g_pool_env = [] {
+  const char* e = std::getenv("DSV_POOL");
+  return !(e && e[0] == '0');
+}();
+
+void pool_free_entry(const PoolEntry& e) {
+  DeviceGuard g(e.device);
+  cudaFree(e.ptr);
+  if (e.scratch) cudaFree(e.scratch);
+  if (e.gdata) cudaFree(e.gdata);
+  if (e.stream) cudaStreamDestroy(e.stream);
+}
+
+bool pool_take(int dev, size_t bytes, PoolEntry* out) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (size_t i = 0; i < g_pool.size(); ++i)
+    if (g_pool[i].device == dev && g_pool[i].bytes == bytes) {
+      *out = g_pool[i];
+      g_pool.erase(g_pool.begin() + long(i));
+      return true;
+    }
+  return false;
+}
+
+void pool_put(const PoolEntry& e) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool.push_back(e);
+  if (g_pool.size() > kPoolMaxEntries) {  // oldest out
+    pool_free_entry(g_pool.front());
+    g_pool.erase(g_pool.begin());
+  }
+}
+
+void pool_release_dev(int dev) {  // dev < 0: all devices
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (size_t i = 0; i < g_pool.size();) {
+    if (dev < 0 || g_pool[i].device == dev) {
+      pool_free_entry(g_pool[i]);
+      g_pool.erase(g_pool.begin() + long(i));
+    } else {
+      ++i;
+    }
+  }
+}
+}  // namespace
+
+int dsv_pool_release(int device) {
+  pool_release_dev(device);
+  return DSV_OK;
+}
+
 int dsv_state_create(int device, int nbits, int dtype, dsv_state** out) {
   if (!out) return fail(DSV_EINVAL, "null out");
   *out = nullptr;
@@ -597,7 +671,26 @@ int dsv_state_create(int device, int nbits, int dtype, dsv_state** out) {
   s->nbits = nbits;
   s->dtype = dtype;
   const size_t bytes = amp_bytes(dtype) << nbits;
-  cudaError_t e = cudaMalloc(&s->d, bytes);
+  cudaError_t e = cudaSuccess;
+  PoolEntry pe;
+  if (g_pool_env && pool_take(device, bytes, &pe)) {
+    s->d = pe.ptr;
+    s->stream = pe.stream;
+    s->scratch = pe.scratch;
+    s->scratch_bytes = pe.scratch_bytes;
+    s->gdata = pe.gdata;
+    s->gdata_bytes = pe.gdata_bytes;
+    *out = s;
+    return dsv_set_basis(s, 0);
+  }
+  {
+    e = cudaMalloc(&s->d, bytes);
+    if (e == cudaErrorMemoryAllocation) {  // cached buffers may be holding the memory
+      cudaGetLastError();
+      pool_release_dev(device);
+      e = cudaMalloc(&s->d, bytes);
+    }
+  }
   if (e != cudaSuccess) {
     delete s;
     return cuda_fail(e, "cudaMalloc(state)");
@@ -623,6 +716,12 @@ int dsv_state_destroy(dsv_state* s) {
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   for (auto e : s->uev)
     if (e) cudaEventDestroy(e);
+  if (s->d && s->owned && !s->ipc && !s->exported && g_pool_env) {
+    pool_put({s->device, amp_bytes(s->dtype) << s->nbits, s->d, s->stream, s->scratch, s->scratch_bytes, s->gdata,
+              s->gdata_bytes});
+    delete s;
+    return DSV_OK;
+  }
   if (s->scratch) cudaFree(s->scratch);
   if (s->gdata) cudaFree(s->gdata);
   if (s->d) {
@@ -1454,6 +1553,7 @@ int dsv_ipc_handle(dsv_state* s, void* out64) {
   DeviceGuard g(s->device);
   cudaIpcMemHandle_t h;
   CK(cudaIpcGetMemHandle(&h, s->d));
+  s->exported = true;
   static_assert(sizeof(h) == 64, "IPC handle size");
   std::memcpy(out64, &h, 64);
   return DSV_OK;
