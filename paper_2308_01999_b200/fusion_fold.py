@@ -143,8 +143,10 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
     ops: list = []
     prov: list[list[int]] = []
 
+    qsets = [frozenset(g.qubits) for g in gates]  # computed once: the scan below revisits gates
+
     def qset(i):
-        return set(gates[i].qubits)
+        return qsets[i]
 
     while True:
         g0 = next((i for i in remaining if phases[i] is None), None)
