@@ -17,6 +17,7 @@ namespace dsv {
 template <int K, typename R>
 struct DenseP {
   Geom g;
+  int cached;  // members share 128-byte lines (low targets): L1-cached loads, not streaming
   uint64_t offs[1 << K];
   cplx<R> m[(1 << K) * (1 << K)];
   R msum[(1 << K) * (1 << K)];  // re + im of m (3-multiplication products)
@@ -45,7 +46,7 @@ k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __r
     base[it] = expand(p.g, w);
     if (w < p.g.nwork) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) in[it][j] = ldg_s(sv + base[it] + p.offs[j]);
+      for (int j = 0; j < D; ++j) in[it][j] = p.cached ? __ldg(sv + base[it] + p.offs[j]) : ldg_s(sv + base[it] + p.offs[j]);
     }
   }
 #pragma unroll
@@ -90,7 +91,12 @@ static cudaError_t dense_reg_t(const Geom& g, const uint64_t* offs, const void* 
   constexpr int ITEMS = DenseItems<VT, K>::value;
   DenseP<K, R> p;
   p.g = g;
-  for (int j = 0; j < D; ++j) p.offs[j] = offs[j];
+  uint64_t span = 0;
+  for (int j = 0; j < D; ++j) {
+    p.offs[j] = offs[j];
+    span |= offs[j];
+  }
+  p.cached = span != 0 && span * sizeof(typename VT::V) < 256;
   const cplx<R>* m = static_cast<const cplx<R>*>(matrix);
   for (int i = 0; i < D * D; ++i) {
     p.m[i] = m[i];
@@ -223,7 +229,12 @@ static cudaError_t expect_dense_t(const Geom& g, const uint64_t* offs, const voi
   constexpr int D = 1 << K;
   DenseP<K, R> p;
   p.g = g;
-  for (int j = 0; j < D; ++j) p.offs[j] = offs[j];
+  uint64_t span = 0;
+  for (int j = 0; j < D; ++j) {
+    p.offs[j] = offs[j];
+    span |= offs[j];
+  }
+  p.cached = span != 0 && span * sizeof(typename VT::V) < 256;
   const cplx<R>* m = static_cast<const cplx<R>*>(matrix);
   for (int i = 0; i < D * D; ++i) p.m[i] = m[i];
   uint64_t blocks = (g.nwork + 255) / 256;
