@@ -1229,6 +1229,35 @@ int dsv_swap_index_bits(dsv_state* s, const int32_t* pairs, int npairs) {
     for (int q = 0; q < sp.np; ++q) { sp.a[q] -= 1; sp.b[q] -= 1; }
   }
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)) * (1.0 - std::ldexp(1.0, -sp.np));
+  const int ubits = s->nbits - (mode == MODE_VEC2 ? 1 : 0);
+  if (sp.np <= 3 && ubits - 2 * sp.np >= 0) {
+    SwapGeomP gp;
+    std::memset(&gp, 0, sizeof gp);
+    std::vector<int> holes;
+    for (int q = 0; q < sp.np; ++q) {
+      holes.push_back(sp.a[q]);
+      holes.push_back(sp.b[q]);
+    }
+    std::sort(holes.begin(), holes.end());
+    if (int rc = make_geom(ubits, holes, 0, &gp.g)) return rc;
+    for (uint32_t pat = 0; pat < (1u << (2 * sp.np)); ++pat) {
+      uint64_t i = 0, j = 0;
+      for (int q = 0; q < sp.np; ++q) {
+        const uint64_t xa = pat >> (2 * q) & 1, xb = pat >> (2 * q + 1) & 1;
+        i |= xa << sp.a[q] | xb << sp.b[q];
+        j |= xb << sp.a[q] | xa << sp.b[q];  // the pair's two bits exchanged
+      }
+      if (j > i) {
+        gp.oi[gp.nsw] = i;
+        gp.oj[gp.nsw] = j;
+        ++gp.nsw;
+      }
+    }
+    ProfTok t = prof_start(s);
+    CKL(launch_swap_geom(s->dtype, mode, gp, s->d, s->stream), 1);
+    prof_stop(s, t, PC_SWAP, bytes);
+    return DSV_OK;
+  }
   ProfTok t = prof_start(s);
   CKL(launch_swap_bits(s->dtype, mode, nunits, sp, s->d, s->stream), 1);
   prof_stop(s, t, PC_SWAP, bytes);

@@ -97,6 +97,14 @@ struct SwapPairs {
 };
 cudaError_t launch_swap_bits(int dtype, int mode, uint64_t nunits, const SwapPairs& sp, void* sv,
                              cudaStream_t st);
+// p <= 3 pairs: owner enumeration over the non-pair bits (g: holes = pair bits,
+// unit space); oi/oj = unit offsets of the nsw = (4^p - 2^p)/2 owner/partner pairs
+struct SwapGeomP {
+  Geom g;
+  int nsw;
+  uint64_t oi[28], oj[28];
+};
+cudaError_t launch_swap_geom(int dtype, int mode, const SwapGeomP& p, void* sv, cudaStream_t st);
 cudaError_t launch_gather(int dtype, int nbits, const int32_t* ordering, uint64_t begin,
                           uint64_t count, const void* sv, void* d_out, cudaStream_t st);
 cudaError_t launch_scatter(int dtype, int nbits, const int32_t* ordering, uint64_t begin,

@@ -34,6 +34,66 @@ k_swap_bits(typename VT::V* __restrict__ sv, uint64_t nunits, const __grid_const
   }
 }
 
+// Few pairs (p <= 3): enumerate only the orbit owners.  Work items run over
+// the bits outside the pairs (holes = all pair bits), so consecutive threads
+// take consecutive units and every access is a coalesced run; each item swaps
+// its (4^p - 2^p) / 2 owner/partner pairs, ITEMS items in flight per thread.
+template <class VT, int NSW, int ITEMS>
+__global__ void __launch_bounds__(256)
+k_swap_geom(typename VT::V* __restrict__ sv, const __grid_constant__ SwapGeomP p) {
+  using V = typename VT::V;
+  const uint64_t w0 = uint64_t(blockIdx.x) * (256ull * ITEMS) + threadIdx.x;
+  V x[ITEMS][NSW], y[ITEMS][NSW];
+  uint64_t base[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * 256;
+    base[it] = expand(p.g, w);
+    if (w < p.g.nwork) {
+#pragma unroll
+      for (int q = 0; q < NSW; ++q) {
+        x[it][q] = ldg_s(sv + base[it] + p.oi[q]);
+        y[it][q] = ldg_s(sv + base[it] + p.oj[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * 256;
+    if (w >= p.g.nwork) continue;
+#pragma unroll
+    for (int q = 0; q < NSW; ++q) {
+      stg_s(sv + base[it] + p.oi[q], y[it][q]);
+      stg_s(sv + base[it] + p.oj[q], x[it][q]);
+    }
+  }
+}
+
+template <class VT, int NSW>
+static cudaError_t swap_geom_t(const SwapGeomP& p, void* sv, cudaStream_t st) {
+  constexpr int ITEMS = NSW >= 6 ? 1 : 4;
+  const uint64_t blocks = (p.g.nwork + 256ull * ITEMS - 1) / (256ull * ITEMS);
+  if (blocks == 0) return cudaSuccess;
+  k_swap_geom<VT, NSW, ITEMS><<<unsigned(blocks), 256, 0, st>>>(static_cast<typename VT::V*>(sv), p);
+  return cudaGetLastError();
+}
+
+template <class VT>
+static cudaError_t swap_geom_mode(const SwapGeomP& p, void* sv, cudaStream_t st) {
+  switch (p.nsw) {
+    case 1: return swap_geom_t<VT, 1>(p, sv, st);
+    case 6: return swap_geom_t<VT, 6>(p, sv, st);
+    case 28: return swap_geom_t<VT, 28>(p, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_swap_geom(int dtype, int mode, const SwapGeomP& p, void* sv, cudaStream_t st) {
+  if (dtype == 1) return swap_geom_mode<C128x1>(p, sv, st);
+  if (mode == MODE_VEC2) return swap_geom_mode<C64x2>(p, sv, st);
+  return swap_geom_mode<C64x1>(p, sv, st);
+}
+
 static unsigned grid_for(uint64_t n, int per_thread = 1) {
   uint64_t b = (n + 256ull * per_thread - 1) / (256ull * per_thread);
   const uint64_t cap = 148ull * 64;

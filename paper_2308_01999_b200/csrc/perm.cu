@@ -21,6 +21,7 @@ namespace dsv {
 template <int K, typename R>
 struct PermP {
   Geom g;
+  int cached;       // members share 128-byte lines (low targets): L1-cached loads
   uint64_t active;  // bit j set: entry j moves or scales
   uint64_t offs_in[1 << K];
   uint64_t offs_out[1 << K];  // offs[perm[j]]
@@ -50,7 +51,8 @@ k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __res
     if (w < p.g.nwork) {
 #pragma unroll
       for (int j = 0; j < D; ++j)
-        if ((p.active >> j) & 1ull) in[it][j] = ldg_s(sv + base[it] + p.offs_in[j]);
+        if ((p.active >> j) & 1ull)
+          in[it][j] = p.cached ? __ldg(sv + base[it] + p.offs_in[j]) : ldg_s(sv + base[it] + p.offs_in[j]);
     }
   }
 #pragma unroll
@@ -83,6 +85,9 @@ static cudaError_t perm_reg_t(const Geom& g, const uint64_t* offs_in, const uint
   PermP<K, R> p;
   p.g = g;
   p.active = active;
+  uint64_t span = 0;
+  for (int j = 0; j < D; ++j) span |= offs_in[j];
+  p.cached = span != 0 && span * sizeof(typename VT::V) < 256;
   const cplx<R>* d = static_cast<const cplx<R>*>(diag);
   for (int j = 0; j < D; ++j) {
     p.offs_in[j] = offs_in[j];
