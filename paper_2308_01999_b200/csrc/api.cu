@@ -336,12 +336,26 @@ struct PhaseTerm {
 // Can the tensor-core kernel take this gate?  complex64, k in {4, 5}, whole
 // 128-group tiles.  Index bit 0 free selects 16-byte row-pair copies (PAIR),
 // else each thread moves its own row 8 bytes per member.
+// 2: targets exactly bits 0..k-1 and no control below bit k + 7 (tiles of 128
+// groups are contiguous); 1: index bit 0 free; 0: otherwise
+int tc_mode(const GateGeom& gg) {
+  bool low = true;
+  for (int m = 0; m < gg.k; ++m) low = low && gg.tsorted[m] == m;
+  if (low) {
+    for (int b : gg.holes)
+      if (b >= gg.k && b < gg.k + 7) low = false;
+    if (low) return 2;
+  }
+  return gg.holes[0] != 0 ? 1 : 0;
+}
+
 bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
   if (!g_tc_env || s->dtype != DSV_C64) return false;
   if (gg.k < 4 || gg.k > 5) return false;
   // rows are the lowest free bits: with bits 0 and 1 both holes, consecutive
-  // rows sit >= 32 bytes apart and the per-row 8-byte copies waste sectors
-  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1) return false;
+  // rows sit >= 32 bytes apart and the per-row 8-byte copies waste sectors —
+  // unless the targets are exactly bits 0..k-1 (contiguous tiles, mode 2)
+  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1 && tc_mode(gg) != 2) return false;
   const int free_bits = s->nbits - gg.k - gg.nctrl;
   if (free_bits < 7) return false;
   return device_has_tcgen05(s->device);
@@ -357,7 +371,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   TcDesc d;
   std::memset(&d, 0, sizeof d);
   d.g = uv.g;
-  d.pair = gg.holes[0] != 0;
+  d.mode = tc_mode(gg);
   for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
   // phase slots per index nibble: [nnib][16][8]
   int nib_of[16];
@@ -823,8 +837,10 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   DeviceGuard g(s->device);
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * std::ldexp(1.0, s->nbits - nctrl);
   const uint64_t D = 1ull << k;
-  // plain k = 4 stays on the CUDA cores (HBM-bound there: 6.3 TB/s vs 4.8 on the tensor path)
-  if (k == 5 && tc_eligible(s, gg)) return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
+  // plain k = 4 stays on the CUDA cores (HBM-bound there: 6.3 TB/s vs 4.8 on
+  // the tensor path) except on the lowest four bits (CUDA cores: 2 TB/s)
+  if ((k == 5 || (k == 4 && tc_mode(gg) == 2)) && tc_eligible(s, gg))
+    return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
   int nlow = 0;
   for (int m = 0; m < k; ++m) nlow += gg.tsorted[m] < (s->dtype == DSV_C64 ? 4 : 3);

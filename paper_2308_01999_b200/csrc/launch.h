@@ -36,7 +36,8 @@ struct TcDesc {
   Geom g;
   int e_b;
   int coop;  // phase terms avoid the tile's row bits (lowest 7 free bits): one phase vector per tile
-  int pair;  // index bit 0 free: 16-byte copies/stores of adjacent row pairs (else 8 B per row)
+  int mode;  // 0: 8-byte copies of each thread's row, 1: index bit 0 free (16-byte row pairs),
+             // 2: targets = bits 0..k-1 (contiguous tiles, row-major staging)
   int nnib;
   int nib_shift[16];
   uint64_t offs[32];

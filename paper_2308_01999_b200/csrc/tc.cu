@@ -156,7 +156,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
-constexpr int kTcMaxNib = 10;          // phase-table nibbles: index bits < 40
+constexpr int kTcMaxNib = 10;
+constexpr int kTcRow = 0, kTcPair = 1, kTcLow = 2;          // phase-table nibbles: index bits < 40
 constexpr float kMagic = 12582912.f;   // 1.5 * 2^23: (x + kMagic) - kMagic = rint(x), |x| < 2^22
 constexpr float kMagic16 = 49152.f;    // 1.5 * 2^15: rounds to multiples of 2^-8, |x| < 2^14
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -233,11 +234,16 @@ __device__ __forceinline__ void issue_mma(uint32_t sbase) {
 //   wait for tile i's copies; phase-multiply in registers; row exponent
 //   wait MMA(i-1); epilogue(i-1): TMEM accumulators -> HBM
 //   limbs of tile i -> TMEM (A); group barrier; thread 0 issues MMA(i), commit
-template <int K, bool PHASED, bool PAIR>
+template <int K, bool PHASED, int MODE>
 __global__ void __launch_bounds__(256, 1)
 k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, const float4* __restrict__ tab,
            float2* __restrict__ sv) {
   using L = TcLayout<K>;
+  // MODE: kTcRow (8-byte copies/stores of each thread's own row), kTcPair
+  // (index bit 0 free: 16-byte row pairs), kTcLow (targets = bits 0..k-1:
+  // tiles are contiguous, staged row-major with a 16-byte-chunk swizzle)
+  constexpr bool PAIR = MODE == kTcPair;
+  constexpr bool LOWT = MODE == kTcLow;
   constexpr int D = L::D;
   constexpr int N = L::N;
   constexpr int S = L::NSTAGE;
@@ -291,7 +297,15 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
     uint64_t tb = 0;
     if (tl < p.ntiles) {
       tb = expand(p.g, tl * 128);
-      if constexpr (PAIR) {
+      if constexpr (LOWT) {  // contiguous 128 x D amplitudes: chunk q -> row q / (D/2), swizzled column
+        const uint32_t st0 = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE;
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) {
+          const int q = row + 128 * m;
+          const int r = q / (D / 2), c = q % (D / 2);
+          cp_async16(st0 + r * (D * 8) + ((c ^ (r & 7)) << 4), sv + tb + 2 * q);
+        }
+      } else if constexpr (PAIR) {
         const uint64_t b = tb | prowoff;
         const uint32_t dst = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE + prow * 8;
 #pragma unroll
@@ -360,6 +374,22 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1).
   const bool odd = row & 1;
   auto epilogue = [&](uint64_t b, float scale) {
+    if constexpr (LOWT) {  // this row's members are contiguous: 16-byte stores
+#pragma unroll
+      for (int h = 0; h < N / 32; ++h) {
+        float c0[32], c1[32];
+        tmem_ld32(tlane + uint32_t(L::T_ACC0 + h * 32), c0);
+        tmem_ld32(tlane + uint32_t(L::T_ACC12 + h * 32), c1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float o[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o[c] = __fmaf_rn(c1[4 * i + c], 1.f / 256.f, c0[4 * i + c]) * scale;
+          __stcs(reinterpret_cast<float4*>(sv + b) + h * 8 + i, make_float4(o[0], o[1], o[2], o[3]));
+        }
+      }
+      return;
+    }
     if constexpr (!PAIR) {  // 8-byte stores of this row's members
 #pragma unroll
       for (int h = 0; h < N / 32; ++h) {
@@ -408,11 +438,21 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
 #pragma unroll
     for (int s = 0; s + 1 < S - 1; ++s) tq[s] = tq[s + 1];
     tq[S - 2] = tb_new;
-    const float2* raw = reinterpret_cast<const float2*>(sm + L::RING + (grp * S + stage) * L::STAGE) + row;
+    const unsigned char* stg = sm + L::RING + (grp * S + stage) * L::STAGE;
     stage = stage + 1 == S ? 0 : stage + 1;
     float2 v[D];
+    if constexpr (LOWT) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) v[j] = raw[j * 128];
+      for (int c = 0; c < D / 2; ++c) {
+        const float4 x = *reinterpret_cast<const float4*>(stg + row * (D * 8) + ((c ^ (row & 7)) << 4));
+        v[2 * c] = make_float2(x.x, x.y);
+        v[2 * c + 1] = make_float2(x.z, x.w);
+      }
+    } else {
+      const float2* raw = reinterpret_cast<const float2*>(stg) + row;
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = raw[j * 128];
+    }
     if constexpr (PHASED) {
       if (p.coop) {  // the tile's D phase factors, computed last iteration by the last warp
         const float2* P = Pb + (it & 1) * D;
@@ -510,7 +550,7 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   }
 }
 
-template <int K, bool PHASED, bool PAIR>
+template <int K, bool PHASED, int MODE>
 static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
   using L = TcLayout<K>;
   TcP<K> p;
@@ -527,7 +567,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_tc<K, PHASED, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc<K, PHASED, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
@@ -535,7 +575,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   const uint64_t need = (p.ntiles + 1) / 2;        // two tiles in flight per CTA
   if (blocks > need) blocks = need;
   if (blocks == 0) return cudaSuccess;
-  k_dense_tc<K, PHASED, PAIR><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+  k_dense_tc<K, PHASED, MODE><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
                                                               static_cast<const float4*>(d_tab),
                                                               static_cast<float2*>(sv));
   return cudaGetLastError();
@@ -552,8 +592,11 @@ int tc_smem_bytes(int k) {
 template <int K>
 static cudaError_t tc_k(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
   const bool ph = d.nnib > 0;
-  if (d.pair) return ph ? tc_go<K, true, true>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, true>(d, d_bmat, d_tab, sv, st);
-  return ph ? tc_go<K, true, false>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, false>(d, d_bmat, d_tab, sv, st);
+  switch (d.mode) {
+    case kTcPair: return ph ? tc_go<K, true, kTcPair>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, kTcPair>(d, d_bmat, d_tab, sv, st);
+    case kTcLow: return ph ? tc_go<K, true, kTcLow>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, kTcLow>(d, d_bmat, d_tab, sv, st);
+  }
+  return ph ? tc_go<K, true, kTcRow>(d, d_bmat, d_tab, sv, st) : tc_go<K, false, kTcRow>(d, d_bmat, d_tab, sv, st);
 }
 
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,

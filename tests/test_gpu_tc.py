@@ -76,12 +76,14 @@ def test_tc_dense_vs_oracle(k):
         assert _rel_err(got, want) <= REL, (trial, targets, ctrls, _rel_err(got, want))
 
 
-@pytest.mark.parametrize("case", ["bit1", "ctrl0", "spread0"])
+@pytest.mark.parametrize("case", ["low0", "low0c", "bit1", "ctrl0", "spread0"])
 def test_tc_dense_low_bits_vs_oracle(case):
     """Index bit 0 a target or control: the 8-byte-per-row (non-pair) copies."""
     rng = np.random.default_rng(hash(case) % 1000)
     n = 16
     targets, ctrls = {
+        "low0": ([0, 1, 2, 3, 4], []),         # contiguous tiles (row-major staging)
+        "low0c": ([0, 1, 2, 3, 4], [(13, 1)]),
         "bit1": ([1, 2, 3, 9, 14], []),
         "ctrl0": ([2, 5, 8, 11, 15], [(0, 1)]),
         "spread0": ([0, 4, 7, 10, 13], [(15, 0)]),
@@ -106,6 +108,8 @@ def test_tc_phased_vs_oracle(k):
         targets = [int(x) for x in rng.choice(np.arange(2, n), size=k, replace=False)]
         if trial == 3:
             targets[0] = 0  # index bit 0 a target: per-row copies
+        if trial == 2:
+            targets = list(range(k))  # the lowest k bits: contiguous tiles
         outside_bits = [q for q in range(n) if q not in targets]
         cross = [(int(rng.integers(0, k)), int(b), float(rng.uniform(-7, 7)))
                  for b in rng.choice(outside_bits, size=min(12, len(outside_bits)), replace=False)]
