@@ -449,6 +449,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   if (int rc = ensure_gdata(s, host.size())) return rc;
   CK(cudaMemcpyAsync(s->gdata, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
   const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
+  d.htab = reinterpret_cast<const float*>(host.data() + limb_bytes);
   ProfTok t = prof_start(s);
   CKL(launch_dense_tc(k, d, d_b, d_b + limb_bytes, s->d, s->stream), 1);
   prof_stop(s, t, prof_class, bytes);

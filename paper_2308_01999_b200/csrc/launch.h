@@ -36,6 +36,7 @@ struct TcDesc {
   Geom g;
   int e_b;
   int coop;  // phase terms avoid the tile's row bits (lowest 7 free bits): one phase vector per tile
+  const float* htab;  // host copy of the phase table (tile-uniform phases read it from the constant bank)
   int mode;  // 0: 8-byte copies of each thread's row, 1: index bit 0 free (16-byte row pairs),
              // 2: targets = bits 0..k-1 (contiguous tiles, row-major staging)
   int nnib;

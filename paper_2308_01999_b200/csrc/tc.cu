@@ -175,6 +175,10 @@ struct TcP {
   int coop;               // phase uniform over a tile's 128 rows: computed once per tile
   int nib_shift[16];      // amplitude-index shift of nibble c
   uint64_t offs[1 << K];  // member offsets (amplitudes)
+  // tile-uniform (coop) phase table in the kernel-parameter constant bank:
+  // every lane of the computing warp reads the same entries (broadcast), no
+  // global-memory latency on the path to the group barrier
+  float4 ctab[kTcMaxNib * 16 * 2];
 };
 
 template <int K>
@@ -340,13 +344,26 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
     }
   };
   // tile-uniform phases: thread 128 - D + j of the group computes factor j of
-  // the group's tile i (base tb) into buffer i & 1 (published by the next group barrier)
+  // the group's tile i (base tb) into buffer i & 1 (published by a later group barrier)
   float2* Pb = reinterpret_cast<float2*>(sm + L::PBUF) + grp * 2 * D;
+  auto phase_angles_c = [&](uint64_t b, float (&a)[8]) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) a[s] = 0.f;
+#pragma unroll
+    for (int c = 0; c < kTcMaxNib; ++c) {
+      if (c < p.nnib) {
+        const int r = (c * 16 + int((b >> p.nib_shift[c]) & 15u)) * 2;
+        const float4 x = p.ctab[r], y = p.ctab[r + 1];
+        a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+        a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+      }
+    }
+  };
   auto coop_phase = [&](int i, uint64_t tb) {
     const int j = row - (128 - D);
     if (PHASED && p.coop && j >= 0 && tile_of(i) < p.ntiles) {
       float a[8];
-      phase_angles(tb, a);
+      phase_angles_c(tb, a);
       float ang = a[K];
 #pragma unroll
       for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
@@ -359,6 +376,7 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) tq[s] = issue(s);
   coop_phase(0, tq[0]);
+  coop_phase(1, tq[1]);
   cp_async_wait<S - 2>();  // tile 0 landed (this thread's part; the barrier below publishes it)
 
   if (*tmem_slot != 0u) __trap();  // whole-TMEM allocation starts at lane 0, column 0
@@ -374,6 +392,9 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1).
   const bool odd = row & 1;
   auto epilogue = [&](uint64_t b, float scale) {
+#ifdef DSV_AB_NOEPI
+    return;
+#endif
     if constexpr (LOWT) {  // this row's members are contiguous: 16-byte stores
 #pragma unroll
       for (int h = 0; h < N / 32; ++h) {
@@ -509,10 +530,16 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const float x = c ? v[h * 16 + q].y : v[h * 16 + q].x;
+#ifndef DSV_AB_NOSPLIT
           a0[c] = __fadd_rn(__fmaf_rn(x, s8, kMagic), -kMagic);
           const float r1 = __fmaf_rn(a0[c], -256.f, x * s16);
           a1[c] = __fadd_rn(__fadd_rn(r1, kMagic), -kMagic);
           a2[c] = __fadd_rn(__fadd_rn(__fadd_rn(r1, -a1[c]), kMagic16), -kMagic16);
+#else
+          a0[c] = x;
+          a1[c] = x;
+          a2[c] = x;
+#endif
         }
         l0[q] = pack2(a0[0], a0[1]);
         l1[q] = pack2(a1[0], a1[1]);
@@ -522,17 +549,22 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
       tmem_st16(tlane + uint32_t(L::T_A + 1 * D + h * 16), l1);
       tmem_st16(tlane + uint32_t(L::T_A + 2 * D + h * 16), l2);
     }
-    coop_phase(it + 1, tq[0]);
     cp_async_wait<S - 2>();  // tile i+1 landed (this thread's part)
     tmem_wait_st();
     fence_before();
     group_sync(grp);
     if (row == 0) {
       fence_after();
+#ifndef DSV_AB_NOMMA
       if (grp == 0) issue_mma<K, 0>(sbase);
       else issue_mma<K, 1>(sbase);
+#endif
       mma_commit(bar);
     }
+    // two tiles ahead, after the barrier: off the barrier's critical path,
+    // published by the next iteration's barrier (buffer (i + 2) & 1 = i & 1
+    // was read before this iteration's barrier)
+    coop_phase(it + 2, tq[S - 2 >= 1 ? 1 : 0]);
     prev_base = base;
     prev_scale = scale;
   }
@@ -562,6 +594,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   p.coop = d.coop;
   for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
+  if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));
   const int smem = L::BYTES + 1024;
   static bool attr_set[64] = {false};
   int dev = 0;
