@@ -351,7 +351,8 @@ int tc_mode(const GateGeom& gg) {
 
 bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
   if (!g_tc_env || s->dtype != DSV_C64) return false;
-  if (gg.k < 4 || gg.k > 5) return false;
+  if (gg.k < 4 || gg.k > 6) return false;
+  if (gg.k == 6 && gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1) return false;  // no contiguous-tile mode at k = 6
   // rows are the lowest free bits: with bits 0 and 1 both holes, consecutive
   // rows sit >= 32 bytes apart and the per-row 8-byte copies waste sectors —
   // unless the targets are exactly bits 0..k-1 (contiguous tiles, mode 2)
@@ -407,14 +408,15 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   // [b0, b1, b2 / 2^8, b1 / 2^8][n][64] (tc.cu)
   std::vector<cplx<float>> m;
   canon_matrix<float>(gg, matrix, m);
-  const int KP = 64;  // one 128-byte bf16 row per B row (2^(k+1) <= 64)
+  const int KP = KK < 64 ? 64 : KK;  // whole 128-byte bf16 K blocks per B row
+  const int nlimb = k == 6 ? 3 : 4;  // k = 6: b0, b1, b2 / 2^8 (a1 / 2^8 rides on the A side)
   float bmax = 0.f;
   for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
   int e_b = 0;
   if (bmax > 0.f) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
   d.e_b = e_b;
   const size_t limb_elems = size_t(KK) * KP;
-  std::vector<uint16_t> limbs(4 * limb_elems, 0);
+  std::vector<uint16_t> limbs(size_t(nlimb) * limb_elems, 0);
   auto bf16_bits = [](float x) {
     uint32_t u;
     std::memcpy(&u, &x, 4);
@@ -436,7 +438,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
           limbs[at] = bf16_bits(float(b0));
           limbs[limb_elems + at] = bf16_bits(float(b1));
           limbs[2 * limb_elems + at] = bf16_bits(float(b2 / 256.0));
-          limbs[3 * limb_elems + at] = bf16_bits(float(b1 / 256.0));
+          if (nlimb > 3) limbs[3 * limb_elems + at] = bf16_bits(float(b1 / 256.0));
         }
     }
   const size_t limb_bytes = (limbs.size() * 2 + 255) / 256 * 256;
@@ -451,7 +453,10 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
   d.htab = reinterpret_cast<const float*>(host.data() + limb_bytes);
   ProfTok t = prof_start(s);
-  CKL(launch_dense_tc(k, d, d_b, d_b + limb_bytes, s->d, s->stream), 1);
+  if (k == 6)
+    CKL(launch_dense_tc6(d, d_b, d_b + limb_bytes, s->d, s->stream), 1);
+  else
+    CKL(launch_dense_tc(k, d, d_b, d_b + limb_bytes, s->d, s->stream), 1);
   prof_stop(s, t, prof_class, bytes);
   return DSV_OK;
 }
@@ -840,7 +845,7 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   const uint64_t D = 1ull << k;
   // plain k = 4 stays on the CUDA cores (HBM-bound there: 6.3 TB/s vs 4.8 on
   // the tensor path) except on the lowest four bits (CUDA cores: 2 TB/s)
-  if ((k == 5 || (k == 4 && tc_mode(gg) == 2)) && tc_eligible(s, gg))
+  if ((k == 5 || k == 6 || (k == 4 && tc_mode(gg) == 2)) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
   int nlow = 0;
@@ -951,7 +956,7 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
                             int ncross, const int32_t* out_b, const double* out_theta, int nout) {
   if (int rc = check_state(s)) return rc;
   if (!matrix) return fail(DSV_EINVAL, "null matrix");
-  if (k < 1 || k > kDenseRegMaxK) return fail(DSV_EUNSUPPORTED, "phased window arity %d outside [1, 5]", k);
+  if (k < 1 || k > 6) return fail(DSV_EUNSUPPORTED, "phased window arity %d outside [1, 6]", k);
   if (ncross < 0 || nout < 0) return fail(DSV_EINVAL, "negative term count");
   GateGeom gg;
   if (int rc = validate_gate(s, targets, k, nullptr, nullptr, 0, &gg)) return rc;
@@ -976,6 +981,8 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
   DeviceGuard g(s->device);
   if (tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  if (k > kDenseRegMaxK)  // the host layer then applies the phases as diagonal gates
+    return fail(DSV_EUNSUPPORTED, "phased 6-qubit window needs the tensor-core path (complex64, >= 7 free bits)");
   if (low_eligible(s, gg))
     return apply_low(s, gg, matrix, terms, PC_DENSE_LOW, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
   UnitView uv;

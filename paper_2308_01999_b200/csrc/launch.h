@@ -41,11 +41,14 @@ struct TcDesc {
              // 2: targets = bits 0..k-1 (contiguous tiles, row-major staging)
   int nnib;
   int nib_shift[16];
-  uint64_t offs[32];
+  uint64_t offs[64];
 };
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);
 int tc_smem_bytes(int k);
+// k = 6 complex64 window on the tensor cores (tc6.cu); d_bmat = [3 limbs:
+// b0, b1, b2 / 2^8][128 rows][128 cols] bf16; modes 0 (rows) and 1 (pairs)
+cudaError_t launch_dense_tc6(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st);
 // k = 1..3 complex64 gate (optionally phased) whose targets are exactly the
 // lowest k bits: 2^(k-1) lanes per group, one float4 each.  g enumerates
 // groups (holes = targets + controls), g.nwork * 2^(k-1) a multiple of 32;

@@ -19,6 +19,8 @@ from __future__ import annotations
 import struct
 from collections.abc import Sequence
 
+import cmath
+
 import numpy as np
 
 from . import _native as N
@@ -165,7 +167,21 @@ class StateVector:
         cross = [(pos[a], self._bits([b])[0], t) for a, b, t in op.cross]
         outside = [(self._bits([b])[0], t) for b, t in op.outside]
         self._sync_in()
-        self._dev.apply_matrix_phased(np.asarray(op.matrix, dtype=self.dtype), bits, cross, outside)
+        m = np.asarray(op.matrix, dtype=self.dtype)
+        try:
+            self._dev.apply_matrix_phased(m, bits, cross, outside)
+        except RuntimeError as e:
+            if "tensor-core path" not in str(e):
+                raise
+            # 6-qubit window off the tensor path: the phase polynomial as
+            # diagonal gates (cross terms on (target, outside) pairs, outside
+            # terms on single bits), then the window matrix
+            for mpos, b, t in cross:
+                self._dev.apply_genperm(np.arange(4), np.array([1, 1, 1, cmath.exp(1j * t)], self.dtype),
+                                        [bits[mpos], b])
+            for b, t in outside:
+                self._dev.apply_genperm(np.arange(2), np.array([1, cmath.exp(1j * t)], self.dtype), [b])
+            self._dev.apply_matrix(m, bits)
         self._mutated()
 
     def apply_matrix(self, g: DenseGate) -> None:

@@ -202,3 +202,75 @@ def test_low_phased_vs_oracle(k):
         sv._mutated()
         assert nat.prof_read().get("dense_low", {}).get("count", 0) == 1
         assert _rel_err(sv.amplitudes, want) <= 2 * REL, (trial, _rel_err(sv.amplitudes, want))
+
+
+# ---- k = 6 windows (tc6.cu) -------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["high", "mid", "spread", "bit0", "ctrl"])
+def test_tc6_dense_vs_oracle(case):
+    rng = np.random.default_rng(600 + len(case))
+    n = 17
+    targets, ctrls = {
+        "high": (list(range(11, 17)), []),
+        "mid": ([4, 5, 6, 7, 8, 9], []),
+        "spread": ([2, 5, 8, 11, 13, 16], []),
+        "bit0": ([0, 3, 6, 9, 12, 15], []),        # per-row 8-byte copies
+        "ctrl": ([3, 6, 7, 9, 12, 14], [(16, 1)]),
+    }[case]
+    targets = [int(t) for t in rng.permutation(targets)]
+    st = random_state(n, rng, np.complex64)
+    m = G.random_unitary(64, rng)
+    want = st.astype(np.complex128)
+    O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), targets, ctrls)
+    sv = StateVector.from_amplitudes(st)
+    nat = _tc_launches(sv)
+    sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
+    assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1
+    assert _rel_err(sv.amplitudes, want) <= REL, _rel_err(sv.amplitudes, want)
+
+
+def test_tc6_phased_and_fold_qft():
+    rng = np.random.default_rng(66)
+    n = 16
+    for targets in ([2, 4, 6, 8, 10, 12], [10, 11, 12, 13, 14, 15]):
+        outside_bits = [q for q in range(n) if q not in targets]
+        cross = [(int(rng.integers(0, 6)), int(b), float(rng.uniform(-7, 7)))
+                 for b in rng.choice(outside_bits, size=8, replace=False)]
+        outside = [(int(b), float(rng.uniform(-7, 7))) for b in rng.choice(outside_bits, size=3, replace=False)]
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(64, rng).astype(np.complex64)
+        want = st.astype(np.complex128) * np.exp(1j * _phase_angles(n, targets, cross, outside))
+        O.apply_dense(want, n, m.astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        sv.native.apply_matrix_phased(m, targets, cross, outside)
+        sv._mutated()
+        assert _rel_err(sv.amplitudes, want) <= 2 * REL
+    # folded QFT at k = 6 (tensor-core 6-qubit windows) = DFT column
+    from paper_2308_01999_b200.circuits import gen_qft, to_gates
+    from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+    n, x = 18, 54321
+    st = np.zeros(1 << n, np.complex64)
+    st[x] = 1
+    sv = StateVector.from_amplitudes(st)
+    for op in fuse_fold(to_gates(gen_qft(n)), 6).ops:
+        sv.apply(op)
+    y = np.arange(1 << n)
+    dft = np.exp(2j * np.pi * x * y / (1 << n)) / np.sqrt(1 << n)
+    assert np.abs(sv.logical_amplitudes() - dft).max() < 2e-6
+
+
+def test_phased_k6_off_tensor_path_falls_back():
+    """Complex128 (no tensor path): the host applies the phases as diagonals."""
+    from paper_2308_01999_b200.circuits import gen_qft, to_gates
+    from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+    n = 12
+    st = np.zeros(1 << n, np.complex128)
+    st[77] = 1
+    sv = StateVector.from_amplitudes(st)
+    for op in fuse_fold(to_gates(gen_qft(n)), 6).ops:
+        sv.apply(op)
+    y = np.arange(1 << n)
+    dft = np.exp(2j * np.pi * 77 * y / (1 << n)) / np.sqrt(1 << n)
+    assert np.abs(sv.logical_amplitudes() - dft).max() < 1e-12

@@ -60,10 +60,10 @@ def main():
     sv = StateVector(n, dtype=np.complex64)
     rng = np.random.default_rng(0)
     out = []
-    for k in (4, 5):
+    for k in (4, 5, 6):
         for label, targets in (("high", list(range(n - k, n))), ("mid", list(range(12, 12 + k))),
-                               ("low2", list(range(2, 2 + k))), ("spread", [2, 9, 15, 22, n - 1][:k]),
-                               ("low0", list(range(k))), ("with0", [0, 7, 13, 20, 25][:k])):
+                               ("low2", list(range(2, 2 + k))), ("spread", [2, 9, 15, 22, 26, n - 1][:k] if k == 6 else [2, 9, 15, 22, n - 1][:k]),
+                               ("low0", list(range(k))), ("with0", [0, 7, 13, 20, 25, 28][:k])):
             g = G.DenseGate(G.random_unitary(1 << k, rng), tuple(targets))
             if args.only not in f"dense{k}_{label}":
                 continue
@@ -74,7 +74,7 @@ def main():
         if args.only in f"dense{k}_low0":
             ms, byts = time_op(sv, g)
             out.append(entry(f"dense{k}_low0", ms, byts, pk, targets=list(range(k))))
-    for k in (3, 4, 5):
+    for k in (3, 4, 5, 6):
         ops = [op for op in fuse_fold(to_gates(gen_qft(n)), k).ops if type(op).__name__ != "QubitSwap"]
         for i, op in enumerate(ops):
             if args.only not in f"qft{n}_fold{k}_op{i}" and not (args.only == "low" and 0 in op.targets):
