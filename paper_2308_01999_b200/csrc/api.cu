@@ -52,6 +52,12 @@ const bool g_low_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// Warp-transpose kernel for dense gates inside the lowest 6 bits (wt.cu); DSV_WT=0 disables.
+const bool g_wt_env = [] {
+  const char* e = std::getenv("DSV_WT");
+  return !(e && e[0] == '0');
+}();
+
 int fail(int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -97,12 +103,12 @@ struct DeviceGuard {
 enum ProfClass {
   PC_DENSE = 0, PC_DENSE_GENERIC, PC_PERM, PC_PERM_GENERIC, PC_SWAP, PC_REDUCE,
   PC_EXPECT, PC_PAULI, PC_COLLAPSE, PC_EXCHANGE, PC_ACCESS, PC_SAMPLE,
-  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE, PC_DENSE_TC, PC_DENSE_LOW
+  PC_DENSE_PHASED, PC_DIAG, PC_DENSE_TILE, PC_DENSE_TC, PC_DENSE_LOW, PC_DENSE_WT
 };
 const char* kProfNames[DSV_PROF_NCLASS] = {
     "dense", "dense_generic", "genperm", "genperm_generic", "swap_bits", "reduce",
     "expect", "pauli", "collapse", "exchange", "access", "sample",
-    "dense_phased", "diag", "dense_tile", "dense_tc", "dense_low"};
+    "dense_phased", "diag", "dense_tile", "dense_tc", "dense_low", "dense_wt"};
 
 struct ProfRec {
   int cls;
@@ -374,29 +380,37 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   d.g = uv.g;
   d.mode = tc_mode(gg);
   for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
-  // phase slots per index nibble: [nnib][16][8]
-  int nib_of[16];
-  for (int c = 0; c < 16; ++c) nib_of[c] = -1;
-  for (const PhaseTerm& t : terms) {
-    const int c = t.bit / 4;
-    if (c >= 10) return fail(DSV_EUNSUPPORTED, "tensor-core phase table covers index bits < 40");
-    if (nib_of[c] < 0) {
-      nib_of[c] = d.nnib;
-      d.nib_shift[d.nnib++] = 4 * c;
-    }
-  }
-  {  // tile rows = the lowest 7 free (non-hole) index bits
-    uint64_t hole_mask = 0, row_mask = 0;
+  // tile rows = the lowest 7 free (non-hole) index bits
+  uint64_t row_mask = 0;
+  {
+    uint64_t hole_mask = 0;
     for (int b : gg.holes) hole_mask |= 1ull << b;
     for (int b = 0, got = 0; b < s->nbits && got < 7; ++b)
       if (!(hole_mask >> b & 1)) {
         row_mask |= 1ull << b;
         ++got;
       }
-    d.coop = 1;
-    for (const PhaseTerm& t : terms)
-      if (row_mask >> t.bit & 1) d.coop = 0;
   }
+  // phase slots per index nibble: [nnib][16][8]; nibbles holding a term on a
+  // row bit come first (d.nnib_row of them: the per-row lookups), the rest are
+  // uniform over a tile (coop = no per-row nibble at all)
+  int nib_of[16];
+  for (int c = 0; c < 16; ++c) nib_of[c] = -1;
+  uint32_t rowvar = 0, used = 0;
+  for (const PhaseTerm& t : terms) {
+    const int c = t.bit / 4;
+    if (c >= 10) return fail(DSV_EUNSUPPORTED, "tensor-core phase table covers index bits < 40");
+    used |= 1u << c;
+    if (row_mask >> t.bit & 1) rowvar |= 1u << c;
+  }
+  for (int pass = 0; pass < 2; ++pass)
+    for (int c = 0; c < 10; ++c)
+      if ((used >> c & 1) && ((rowvar >> c & 1) == (pass == 0 ? 1u : 0u))) {
+        nib_of[c] = d.nnib;
+        d.nib_shift[d.nnib++] = 4 * c;
+        if (pass == 0) ++d.nnib_row;
+      }
+  d.coop = d.nnib_row == 0 ? 1 : 0;
   std::vector<double> tab(size_t(d.nnib) * 16 * 8, 0.0);
   for (const PhaseTerm& t : terms) {
     const int ci = nib_of[t.bit / 4], bb = t.bit % 4;
@@ -848,6 +862,28 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   if ((k == 5 || k == 6 || (k == 4 && tc_mode(gg) == 2)) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
+  if (g_wt_env && nctrl == 0 && k >= 1 && k <= (s->dtype == DSV_C128 ? 3 : 4) && gg.tsorted[k - 1] < 6 &&
+      s->nbits >= 10) {
+    // the register path strides lanes >= 32 bytes apart here: transpose through smem
+    // measured weak layouts of the register path (tools/lowsweep.py, c128_bench.py):
+    // complex64 targets {1,2,3} (0.59 -> 0.95), complex128 {0,1,2} (0.60 -> 0.76)
+    const bool weak = k == 3 && (s->dtype == DSV_C128 ? gg.tsorted[0] == 0 && gg.tsorted[2] == 2
+                                                      : gg.tsorted[0] == 1 && gg.tsorted[2] == 3);
+    if (weak) {
+      ProfTok t = prof_start(s);
+      if (s->dtype == DSV_C128) {
+        std::vector<cplx<double>> m;
+        canon_matrix<double>(gg, matrix, m);
+        CKL(launch_dense_wt(s->dtype, s->nbits, k, gg.tsorted.data(), m.data(), s->d, s->stream), 1);
+      } else {
+        std::vector<cplx<float>> m;
+        canon_matrix<float>(gg, matrix, m);
+        CKL(launch_dense_wt(s->dtype, s->nbits, k, gg.tsorted.data(), m.data(), s->d, s->stream), 1);
+      }
+      prof_stop(s, t, PC_DENSE_WT, bytes);
+      return DSV_OK;
+    }
+  }
   int nlow = 0;
   for (int m = 0; m < k; ++m) nlow += gg.tsorted[m] < (s->dtype == DSV_C64 ? 4 : 3);
   if (k >= 2 && k <= 5 && nlow >= 2 && s->nbits >= 14 && !g_disable_tile) {

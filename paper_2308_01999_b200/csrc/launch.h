@@ -36,6 +36,7 @@ struct TcDesc {
   Geom g;
   int e_b;
   int coop;  // phase terms avoid the tile's row bits (lowest 7 free bits): one phase vector per tile
+  int nnib_row;  // leading phase-table nibbles that vary over a tile's rows (0 when coop)
   const float* htab;  // host copy of the phase table (tile-uniform phases read it from the constant bank)
   int mode;  // 0: 8-byte copies of each thread's row, 1: index bit 0 free (16-byte row pairs),
              // 2: targets = bits 0..k-1 (contiguous tiles, row-major staging)
@@ -62,6 +63,10 @@ struct LowDesc {
 };
 cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const void* d_tab, void* sv,
                              cudaStream_t st);
+// k <= 3 (complex128) / 4 (complex64) dense gate, all targets < 6, no controls:
+// per-warp shared-memory transpose of contiguous runs (tb = sorted target bits)
+cudaError_t launch_dense_wt(int dtype, int nbits, int k, const int* tb, const void* matrix, void* sv,
+                            cudaStream_t st);
 // k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem
 struct TileDesc {
   Geom g;              // tile bases (holes: bits [0,T), high targets, controls >= T)

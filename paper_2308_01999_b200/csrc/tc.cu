@@ -51,6 +51,7 @@ struct TcP {
   int nnib;               // phase-table nibbles (0: plain dense)
   int e_b;                // gate limb exponent: |B| < 2^e_b
   int coop;               // phase uniform over a tile's 128 rows: computed once per tile
+  int nnib_row;           // leading nibbles that vary over the rows (the rest: tile-uniform sums)
   int nib_shift[16];      // amplitude-index shift of nibble c
   uint64_t offs[1 << K];  // member offsets (amplitudes)
   // tile-uniform (coop) phase table in the kernel-parameter constant bank:
@@ -239,6 +240,25 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   };
   auto coop_phase = [&](int i, uint64_t tb) {
     const int j = row - (128 - D);
+    if (PHASED && !p.coop && j == 0 && tile_of(i) < p.ntiles) {
+      // per-row phases: the tile-uniform part of the angle sums (nibbles past
+      // the row-varying ones) once per tile, from the constant bank
+      float a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) a[s] = 0.f;
+#pragma unroll
+      for (int c = 0; c < kTcMaxNib; ++c) {
+        if (c >= p.nnib_row && c < p.nnib) {
+          const int r = (c * 16 + int((tb >> p.nib_shift[c]) & 15u)) * 2;
+          const float4 x = p.ctab[r], y = p.ctab[r + 1];
+          a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+          a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+        }
+      }
+      float4* hb = reinterpret_cast<float4*>(Pb + (i & 1) * D);
+      hb[0] = make_float4(a[0], a[1], a[2], a[3]);
+      hb[1] = make_float4(a[4], a[5], a[6], a[7]);
+    }
     if (PHASED && p.coop && j >= 0 && tile_of(i) < p.ntiles) {
       float a[8];
       phase_angles_c(tb, a);
@@ -361,8 +381,21 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
           v[j] = make_float2(x.x * f.x - x.y * f.y, x.x * f.y + x.y * f.x);
         }
       } else {
+        // tile-uniform part (computed two tiles ahead) + this row's nibbles
         float a[8];
-        phase_angles(base, a);
+        const float4* hb = reinterpret_cast<const float4*>(Pb + (it & 1) * D);
+        const float4 h0 = hb[0], h1 = hb[1];
+        a[0] = h0.x; a[1] = h0.y; a[2] = h0.z; a[3] = h0.w;
+        a[4] = h1.x; a[5] = h1.y; a[6] = h1.z; a[7] = h1.w;
+#pragma unroll
+        for (int c = 0; c < kTcMaxNib; ++c) {
+          if (c < p.nnib_row) {
+            const int r = (c * 16 + int((base >> p.nib_shift[c]) & 15u)) * 2;
+            const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);
+            a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+            a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+          }
+        }
         float2 P[D];
         sincos_red(a[K], &P[0].y, &P[0].x);
 #pragma unroll
@@ -470,6 +503,7 @@ static cudaError_t tc_go(const TcDesc& d, const void* d_bmat, const void* d_tab,
   p.nnib = d.nnib;
   p.e_b = d.e_b;
   p.coop = d.coop;
+  p.nnib_row = d.nnib_row;
   for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
   if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));

@@ -274,3 +274,26 @@ def test_phased_k6_off_tensor_path_falls_back():
     y = np.arange(1 << n)
     dft = np.exp(2j * np.pi * 77 * y / (1 << n)) / np.sqrt(1 << n)
     assert np.abs(sv.logical_amplitudes() - dft).max() < 1e-12
+
+
+# ---- warp-transpose kernel: dense gates inside the lowest 6 bits (wt.cu) --------------------
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_wt_low_targets_vs_oracle(dtype):
+    rng = np.random.default_rng(31)
+    n = 14
+    cases = [[1, 2, 3], [1, 3, 5], [2, 4]] if dtype == np.complex64 else [[0, 1, 2], [0, 2], [1, 2, 5]]
+    for targets in cases:
+        targets = [int(t) for t in rng.permutation(targets)]
+        st = random_state(n, rng, dtype)
+        m = G.random_unitary(1 << len(targets), rng)
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(dtype).astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets)))
+        prof = nat.prof_read()
+        if sorted(targets) in ([1, 2, 3], [0, 1, 2]):
+            assert prof.get("dense_wt", {}).get("count", 0) == 1, prof
+        tol = 2e-6 if dtype == np.complex64 else 1e-13
+        assert _rel_err(sv.amplitudes, want) <= tol, (targets, prof, _rel_err(sv.amplitudes, want))
