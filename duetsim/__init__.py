@@ -8,7 +8,7 @@ device-backed implementations from ``paper_2308_01999_b200`` unchanged.
 import sys as _sys
 
 import paper_2308_01999_b200 as _impl
-from paper_2308_01999_b200 import circuits, core, distsim, fusion, gates, plan, statevec
+from paper_2308_01999_b200 import circuits, cli, core, distsim, fusion, gates, plan, statevec
 from paper_2308_01999_b200 import *  # noqa: F401,F403
 
 for _name, _mod in {
@@ -19,6 +19,7 @@ for _name, _mod in {
     "distsim": distsim,
     "circuits": circuits,
     "plan": plan,
+    "cli": cli,
 }.items():
     _sys.modules[f"{__name__}.{_name}"] = _mod
 

@@ -1,0 +1,80 @@
+"""The simulate CLI (paper_2308_01999_b200/cli.py), mirroring the reference's
+tests/test_cli.py TestSimulate cases for the state-vector engines."""
+
+import json
+
+import numpy as np
+import pytest
+
+from paper_2308_01999_b200.cli import main
+
+
+def run_json(capsys, *argv):
+    code = main(list(argv))
+    out = capsys.readouterr().out
+    return code, json.loads(out)
+
+
+def masked(report):
+    report = dict(report)
+    report.pop("timings", None)
+    return report
+
+
+def test_qft_33_dry_run(capsys):
+    code, rep = run_json(capsys, "simulate", "--circuit", "qft", "--n", "33", "--dry-run")
+    assert code == 0
+    assert rep["counters"]["gates"] == 577
+    assert rep["schema_version"] == 1 and rep["command"] == "simulate"
+
+
+def test_out_of_scope_engine_is_an_error(capsys):
+    assert main(["simulate", "--circuit", "qft", "--n", "4", "--engine", "mps"]) == 1
+
+
+@pytest.mark.gpu
+class TestSimulateGPU:
+    @pytest.fixture(autouse=True)
+    def _gpu(self, gpu_available):
+        return gpu_available
+
+    def test_qft_20_gate_count_and_norm(self, capsys):
+        code, rep = run_json(capsys, "simulate", "--circuit", "qft", "--n", "20", "--engine", "sv")
+        assert code == 0
+        assert rep["counters"]["gates"] == 20 + 190 + 10
+        assert abs(rep["counters"]["norm"] - 1.0) < 1e-10
+        assert rep["timings"]["kernels"]  # per-kernel-class device times
+
+    def test_sv_dist_engine_matches_and_reports_transfers(self, capsys):
+        code, rep = run_json(capsys, "simulate", "--circuit", "qft", "--n", "8", "--engine", "sv-dist",
+                             "--global-bits", "2", "--workers", "2", "--verify")
+        assert code == 0
+        assert rep["verification"]["passed"]
+        assert "transfer_stats" in rep["counters"]
+
+    def test_fusion_flags(self, capsys):
+        code, rep = run_json(capsys, "simulate", "--circuit", "qft", "--n", "8", "--engine", "sv",
+                             "--max-fused-gate-size", "4", "--max-fused-diagonal-gate-size", "6", "--verify")
+        assert code == 0
+        assert rep["counters"]["fused_gates"] < rep["counters"]["gates"]
+        assert rep["verification"]["passed"]
+
+    def test_fold_fusion_c64_on_the_tensor_path(self, capsys):
+        code, rep = run_json(capsys, "simulate", "--circuit", "qft", "--n", "18", "--dtype", "c64",
+                             "--fusion", "fold:5", "--verify")
+        assert code == 0
+        assert rep["verification"]["passed"]
+        assert rep["counters"]["data_passes"] == 4
+        assert "dense_tc" in rep["timings"]["kernels"]
+
+    def test_qaoa_ring_simulation(self, capsys):
+        code, rep = run_json(capsys, "simulate", "--circuit", "qaoa", "--n", "6", "--engine", "sv", "--verify")
+        assert code == 0
+        assert rep["counters"]["gates"] == 6 + 2 * (6 + 6)
+        assert rep["verification"]["passed"]
+
+    def test_deterministic_reports_modulo_timings(self, capsys):
+        args = ("simulate", "--circuit", "qv", "--n", "6", "--engine", "sv", "--seed", "5")
+        _, rep1 = run_json(capsys, *args)
+        _, rep2 = run_json(capsys, *args)
+        assert masked(rep1) == masked(rep2)
