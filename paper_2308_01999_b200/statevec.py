@@ -317,22 +317,45 @@ class StateVector:
         self.bit_map = [relabel.get(bit, bit) for bit in self.bit_map]
 
     # -- serialisation (statevec.py:332-351) --------------------------------------------
+    # streamed file I/O: the file is written / read in
+    # chunks of DUMP_CHUNK amplitudes gathered on the GPU in logical order, so
+    # a 33-qubit state never needs a host copy of the whole vector
+    DUMP_CHUNK = 1 << 24
+
     def dump(self, path) -> None:
         """``<Q`` qubit count, then interleaved little-endian float64 (re, im)
-        in logical order — always float64, also for complex64 states."""
-        data = self.logical_amplitudes().astype(np.complex128)
+        in logical order — always float64, also for complex64 states
+        (statevec.py:332-340 format)."""
+        n = self.num_qubits
+        identity = self.bit_map == list(range(n))
+        self._sync_in()
         with open(path, "wb") as fh:
-            fh.write(struct.pack("<Q", self.num_qubits))
-            fh.write(data.view("<f8").tobytes())
+            fh.write(struct.pack("<Q", n))
+            for begin in range(0, 1 << n, self.DUMP_CHUNK):
+                end = min(1 << n, begin + self.DUMP_CHUNK)
+                if identity:
+                    chunk = self._dev.download(begin=begin, count=end - begin)
+                else:
+                    chunk = self._dev.access_get(list(self.bit_map), begin, end)
+                fh.write(chunk.astype(np.complex128).view("<f8").tobytes())
 
     @classmethod
-    def load(cls, path, device: int | None = None) -> "StateVector":
+    def load(cls, path, device: int | None = None, dtype=np.complex128) -> "StateVector":
+        """Inverse of :meth:`dump` (statevec.py:342-351), streamed into HBM;
+        ``dtype`` may narrow to complex64 on the device."""
+        import os
+
         with open(path, "rb") as fh:
             (n,) = struct.unpack("<Q", fh.read(8))
-            raw = np.frombuffer(fh.read(), dtype="<f8")
-        if raw.size != 2 << n:
-            raise InvalidArgumentError("file length does not match qubit count")
-        return cls.from_amplitudes(raw.view(np.complex128).astype(np.complex128), device=device)
+            if os.fstat(fh.fileno()).st_size != 8 + (16 << n):
+                raise InvalidArgumentError("file length does not match qubit count")
+            sv = cls(n, dtype=dtype, device=device)
+            for begin in range(0, 1 << n, cls.DUMP_CHUNK):
+                count = min(1 << n, begin + cls.DUMP_CHUNK) - begin
+                raw = np.frombuffer(fh.read(16 * count), dtype="<f8")
+                sv._dev.upload(raw.view(np.complex128).astype(sv.dtype), begin=begin)
+        sv._mutated()
+        return sv
 
 
 def run_circuit_sv(gates: Sequence[Gate], num_qubits: int, dtype=np.complex128,
