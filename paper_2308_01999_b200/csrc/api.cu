@@ -1390,16 +1390,81 @@ static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2,
     if (seen >> b & 1) return fail(DSV_EINVAL, "qubits must be distinct");
     seen |= 1ull << b;
   }
-  const bool vec2 = allow_vec2 && s->dtype == DSV_C64 && !(seen & 1ull) && s->nbits >= 1;
+  {  // inner (per-thread) / outer (block-grid) split of the binned bits
+    const int ib_bits = s->dtype == DSV_C64 ? 9 : 8;  // amp bits held by (unit lane, thread index)
+    const int shift1 = s->dtype == DSV_C64 ? 1 : 0;
+    InnerBins ib;
+    std::memset(&ib, 0, sizeof ib);
+    BinGeom bg1;
+    std::memset(&bg1, 0, sizeof bg1);
+    bg1.reg_j = -1;
+    std::vector<int> oholes;
+    // (sampling asks for the per-chunk partials in amplitude-contiguous
+    // chunks of its own size: it keeps the original kernel)
+    bool ok = s->nbits >= ib_bits && d_partial_out == nullptr;
+    for (int j = 0; j < k && ok; ++j) {
+      const int b = bits[j];
+      if (b < ib_bits) {
+        if (ib.n >= 8) {
+          ok = false;
+          break;
+        }
+        ib.pos[ib.n] = b;
+        ib.fin[ib.n++] = j;
+        if (s->dtype == DSV_C64) {
+          if (b == 0) ib.h_binned = 1;
+          else if (b <= 5) ib.lane_mask |= 1u << (b - 1);
+          else ib.warp_mask |= 1u << (b - 6);
+        } else {
+          if (b <= 4) ib.lane_mask |= 1u << b;
+          else ib.warp_mask |= 1u << (b - 5);
+        }
+      } else {
+        ib.ofin[bg1.nb] = j;
+        bg1.bits[bg1.nb++] = b - shift1;
+        oholes.push_back(b - shift1);
+      }
+    }
+    if (ok) {
+      std::sort(oholes.begin(), oholes.end());
+      if (int rc = make_geom(s->nbits - shift1, oholes, 0, &bg1.g)) return rc;
+      bg1.nchunks = chunks_for(bg1.g.nwork);
+      const uint64_t nbins = 1ull << k;
+      const size_t part_bytes = sizeof(double) * nbins * bg1.nchunks;
+      const size_t part_round = ((part_bytes + 255) / 256) * 256;
+      if (int rc = ensure_scratch(s, part_round + sizeof(double) * nbins)) return rc;
+      double* d_partial = static_cast<double*>(s->scratch);
+      double* d_out = reinterpret_cast<double*>(static_cast<char*>(s->scratch) + part_round);
+      ProfTok t = prof_start(s);
+      CKL(launch_probs_in(s->dtype, bg1, ib, s->d, d_partial, s->stream), 1);
+      prof_stop(s, t, PC_REDUCE, double(amp_bytes(s->dtype)) * double(namps(s)));
+      if (d_partial_out) {
+        *d_partial_out = d_partial;
+        *nchunks_out = bg1.nchunks;
+        return DSV_OK;
+      }
+      return finish_reduce(s, nbins, bg1.nchunks, 1, d_partial, d_out, host_out);
+    }
+  }
+  // complex64 with bit 0 binned: float4 units, bit 0 resolved in registers
+  const bool reg0 = s->dtype == DSV_C64 && (seen & 1ull) && s->nbits >= 1;
+  const bool vec2 = (allow_vec2 && s->dtype == DSV_C64 && !(seen & 1ull) && s->nbits >= 1) || reg0;
   const int shift = vec2 ? 1 : 0;
   BinGeom bg;
   std::memset(&bg, 0, sizeof bg);
+  bg.reg_j = -1;
   std::vector<int> holes;
-  for (int b = 0; b < 64; ++b)
+  for (int b = reg0 ? 1 : 0; b < 64; ++b)
     if (seen >> b & 1) holes.push_back(b - shift);
   if (int rc = make_geom(s->nbits - shift, holes, 0, &bg.g)) return rc;
-  bg.nb = k;
-  for (int j = 0; j < k; ++j) bg.bits[j] = bits[j] - shift;
+  bg.nb = 0;
+  for (int j = 0; j < k; ++j) {
+    if (reg0 && bits[j] == 0) {
+      bg.reg_j = j;
+      continue;
+    }
+    bg.bits[bg.nb++] = bits[j] - shift;
+  }
   bg.nchunks = chunks_for(bg.g.nwork);
   const uint64_t nbins = 1ull << k;
   const size_t part_bytes = sizeof(double) * nbins * bg.nchunks;

@@ -140,15 +140,32 @@ cudaError_t launch_pauli(int dtype, int nbits, const PauliOp& op, void* sv, cuda
 // ---- reductions -------------------------------------------------------------
 // probability bins: partial[bin*nchunks + chunk]; bins over `bits` (bit j of bin -> bits[j])
 constexpr int kReduceThreads = 256;
-constexpr int kReduceUnitsPerThread = 16;
+constexpr int kReduceUnitsPerThread = 64;
 struct BinGeom {
   Geom g;            // free-bit expansion (holes = binned bits), in unit space
-  int nb;            // number of binned bits
+  int nb;            // number of binned bits handled by the block grid
   int bits[40];      // unit-space bit of bin bit j
   uint64_t nchunks;  // chunks per bin
+  int reg_j;         // >= 0 (complex64 float4 units): amplitude bit 0 is bin bit reg_j and is
+                     // resolved inside the unit (x,y / z,w); bits[] then lists the other bin bits
 };
 cudaError_t launch_probs(int dtype, int mode, const BinGeom& bg, const void* sv, double* d_partial,
                          cudaStream_t st);
+// low ("inner") binned bits resolved per thread: pos[j] = position of inner bin
+// bit j among (amp bit 0 lane | lane bits | warp bits) — c64: amp bit b -> b,
+// c128: amp bit b -> b; fin[j] / ofin[j] = final bin-index bit of inner /
+// outer bin bit j (outer bins: BinGeom bits, unit space)
+struct InnerBins {
+  int n;
+  int pos[8];
+  int fin[8];
+  int ofin[40];
+  uint32_t lane_mask;  // binned lane bits
+  uint32_t warp_mask;  // binned warp bits
+  int h_binned;        // c64: amplitude bit 0 binned
+};
+cudaError_t launch_probs_in(int dtype, const BinGeom& bg, const InnerBins& ib, const void* sv,
+                            double* d_partial, cudaStream_t st);
 // final reduction: out[b*ncomp + c] = sum_k partial[(b*nchunks + k)*ncomp + c]
 cudaError_t launch_final_sum(uint64_t nbins, uint64_t nchunks, int ncomp, const double* d_partial,
                              double* d_out, cudaStream_t st);

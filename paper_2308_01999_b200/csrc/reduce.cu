@@ -24,6 +24,49 @@ uint64_t chunks_for(uint64_t nunits) {
   return c ? c : 1;
 }
 
+// Amplitude bit 0 binned, complex64: float4 units (coalesced 16-byte loads)
+// and two accumulators, one per value of bit 0 (no strided half-unit reads).
+__global__ void __launch_bounds__(kReduceThreads)
+k_probs_reg0(const float4* __restrict__ sv, const __grid_constant__ BinGeom bg, double* __restrict__ partial) {
+  __shared__ double sh[kReduceThreads / 32];
+  const uint64_t nbins = 1ull << bg.nb;
+  const uint64_t chunk = blockIdx.x / nbins;
+  const uint64_t bin = blockIdx.x % nbins;
+  uint64_t bin_base = 0;
+  for (int j = 0; j < bg.nb; ++j) bin_base |= ((bin >> j) & 1ull) << bg.bits[j];
+  // per-batch sums in fp32 (8 terms), folded into fp64 accumulators: the
+  // fp64 pipe stays off the per-element path
+  double acc0 = 0.0, acc1 = 0.0;
+  const uint64_t f0 = chunk * kChunkUnits + threadIdx.x;
+  constexpr int kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    float4 v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t f = f0 + uint64_t(u0 + u) * kReduceThreads;
+      v[u] = f < bg.g.nwork ? ldg_s(sv + (expand(bg.g, f) | bin_base)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float b0 = 0.f, b1 = 0.f;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      b0 = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, b0));
+      b1 = fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, b1));
+    }
+    acc0 += double(b0);
+    acc1 += double(b1);
+  }
+  const double s0 = block_sum<kReduceThreads>(acc0, sh);
+  const double s1 = block_sum<kReduceThreads>(acc1, sh);
+  if (threadIdx.x == 0) {
+    // full bin index: insert bit 0's value at bin position reg_j
+    const uint64_t lo = bin & ((1ull << bg.reg_j) - 1ull), hi = bin >> bg.reg_j;
+    const uint64_t b0 = lo | (hi << (bg.reg_j + 1));
+    partial[b0 * bg.nchunks + chunk] = s0;
+    partial[(b0 | (1ull << bg.reg_j)) * bg.nchunks + chunk] = s1;
+  }
+}
+
 template <class VT>
 __global__ void __launch_bounds__(kReduceThreads)
 k_probs(const typename VT::V* __restrict__ sv, const __grid_constant__ BinGeom bg,
@@ -65,9 +108,106 @@ k_probs(const typename VT::V* __restrict__ sv, const __grid_constant__ BinGeom b
   if (threadIdx.x == 0) partial[bin * bg.nchunks + chunk] = s;
 }
 
+// Marginals with the low binned bits resolved per thread ("inner" bits: the
+// amplitude bits held by a thread's unit lanes and threadIdx, c64: 0..8,
+// c128: 0..7; a block reads 256 consecutive units per step, so those bits
+// are constant per (thread, lane)).  Outer binned bits (above) select the
+// block's unit subset through the Geom as before.  Per-thread sums: fp32 per
+// batch of 8 units folded into fp64 (complex64) / fp64 (complex128); block
+// reduction in a fixed order (shuffle butterflies over the non-binned lane
+// bits, then per-bin sums over warps): bit-reproducible.
+template <class VT>
+__global__ void __launch_bounds__(kReduceThreads)
+k_probs_in(const typename VT::V* __restrict__ sv, const __grid_constant__ BinGeom bg,
+           const __grid_constant__ InnerBins ib, double* __restrict__ partial) {
+  using V = typename VT::V;
+  using R = typename VT::R;
+  constexpr int L = VT::L;  // amplitudes per unit (amp bit 0 = lane when 2)
+  __shared__ double sm[kReduceThreads / 32][32][2];
+  const uint64_t nouter = 1ull << bg.nb;
+  const uint64_t chunk = blockIdx.x / nouter;
+  const uint64_t ob = blockIdx.x % nouter;
+  uint64_t bin_base = 0;
+  for (int j = 0; j < bg.nb; ++j) bin_base |= ((ob >> j) & 1ull) << bg.bits[j];
+  double acc[2] = {0.0, 0.0};
+  const uint64_t f0 = chunk * kChunkUnits + threadIdx.x;
+  constexpr int kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    V v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t f = f0 + uint64_t(u0 + u) * kReduceThreads;
+      v[u] = f < bg.g.nwork ? ldg_s(sv + (expand(bg.g, f) | bin_base)) : V{};
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      R b = R(0);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        R re, im;
+        VT::get(v[u], l, re, im);
+        b = fma(re, re, fma(im, im, b));
+      }
+      acc[l] += double(b);
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // butterfly over lane bits that are not binned (fixed order)
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    if (!((ib.lane_mask >> i) & 1u)) {
+#pragma unroll
+      for (int l = 0; l < L; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], 1 << i);
+    }
+  }
+  if ((lane & ~ib.lane_mask & 31u) == 0) {
+    sm[warp][lane][0] = acc[0];
+    sm[warp][lane][1] = L == 2 ? acc[1] : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < (1 << ib.n)) {
+    // inner bin t: its binned lane bits, lane slot (bit 0) and warp bits
+    uint32_t lane_b = 0, warp_b = 0, h_b = 0;
+    for (int j = 0; j < ib.n; ++j) {
+      const uint32_t v = (t >> j) & 1u;
+      const int pos = ib.pos[j];  // position in (h | lane << 1 | warp << 6) for c64, (lane | warp << 5) for c128
+      if (L == 2 && pos == 0) h_b = v;
+      else if (pos - (L == 2 ? 1 : 0) < 5) lane_b |= v << (pos - (L == 2 ? 1 : 0));
+      else warp_b |= v << (pos - (L == 2 ? 6 : 5));
+    }
+    double s = 0.0;
+    for (int w = 0; w < kReduceThreads / 32; ++w) {
+      if ((uint32_t(w) & ib.warp_mask) != warp_b) continue;
+      if (L == 2 && !ib.h_binned) s += sm[w][lane_b][0] + sm[w][lane_b][1];
+      else s += sm[w][lane_b][h_b];
+    }
+    // final bin index: inner bit j -> user bit ib.fin[j], outer bit j -> bg.fin... (host packs)
+    uint64_t fb = 0;
+    for (int j = 0; j < ib.n; ++j) fb |= uint64_t((t >> j) & 1) << ib.fin[j];
+    for (int j = 0; j < bg.nb; ++j) fb |= ((ob >> j) & 1ull) << ib.ofin[j];
+    partial[fb * bg.nchunks + chunk] = s;
+  }
+}
+
+cudaError_t launch_probs_in(int dtype, const BinGeom& bg, const InnerBins& ib, const void* sv,
+                            double* d_partial, cudaStream_t st) {
+  const uint64_t blocks = bg.nchunks << bg.nb;
+  if (dtype == 1)
+    k_probs_in<C128x1><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const double2*>(sv), bg, ib, d_partial);
+  else
+    k_probs_in<C64x2><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float4*>(sv), bg, ib, d_partial);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_probs(int dtype, int mode, const BinGeom& bg, const void* sv, double* d_partial,
                          cudaStream_t st) {
   const uint64_t blocks = bg.nchunks << bg.nb;
+  if (bg.reg_j >= 0) {
+    k_probs_reg0<<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float4*>(sv), bg, d_partial);
+    return cudaGetLastError();
+  }
   if (dtype == 1)
     k_probs<C128x1><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const double2*>(sv), bg, d_partial);
   else if (mode == MODE_VEC2)
@@ -109,31 +249,43 @@ k_expect_pauli(const V* __restrict__ sv, uint64_t npairs, const __grid_constant_
   const uint64_t lowmask = h >= 0 ? (1ull << h) - 1ull : 0ull;
   double er = 0.0, ei = 0.0;
   const uint64_t t0 = uint64_t(blockIdx.x) * kChunkUnits + threadIdx.x;
-#pragma unroll 4
-  for (int u = 0; u < kReduceUnitsPerThread; ++u) {
-    const uint64_t t = t0 + uint64_t(u) * kReduceThreads;
-    if (t >= npairs) break;
-    if (h < 0) {
-      const V a = ldg_s(sv + t);
-      const double sg = (__popcll(t & op.yzmask) & 1) ? -1.0 : 1.0;
-      const double p = double(a.x) * double(a.x) + double(a.y) * double(a.y);
-      er = fma(sg, p, er);
-    } else {
-      const uint64_t i = ((t & ~lowmask) << 1) | (t & lowmask);
-      const uint64_t j = i ^ op.xmask;
-      const V a = ldg_s(sv + i);
-      const V b = ldg_s(sv + j);
-      const double ar = a.x, ai = a.y, br = b.x, bi = b.y;
-      const double si = (__popcll(i & op.yzmask) & 1) ? -1.0 : 1.0;
-      const double sj = (__popcll(j & op.yzmask) & 1) ? -1.0 : 1.0;
-      // q = B * b ; term_i = conj(a) * q * si
-      const double qr = op.br * br - op.bi * bi, qi = op.br * bi + op.bi * br;
-      er += si * (ar * qr + ai * qi);
-      ei += si * (ar * qi - ai * qr);
-      // q' = B * a ; term_j = conj(b) * q' * sj
-      const double pr = op.br * ar - op.bi * ai, pi = op.br * ai + op.bi * ar;
-      er += sj * (br * pr + bi * pi);
-      ei += sj * (br * pi - bi * pr);
+  // batches of kBatch pairs: every load of a batch is issued before the first
+  // use (memory-level parallelism), missing tail entries read as zero
+  constexpr int kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    V a[kBatch], b[kBatch];
+    uint64_t ii[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t t = t0 + uint64_t(u0 + u) * kReduceThreads;
+      const bool on = t < npairs;
+      const uint64_t i = h < 0 ? t : (((t & ~lowmask) << 1) | (t & lowmask));
+      ii[u] = i;
+      a[u] = on ? ldg_s(sv + i) : V{};
+      if (h >= 0) b[u] = on ? ldg_s(sv + (i ^ op.xmask)) : V{};
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t i = ii[u];
+      if (h < 0) {
+        const double sg = (__popcll(i & op.yzmask) & 1) ? -1.0 : 1.0;
+        const double pr = double(a[u].x) * double(a[u].x) + double(a[u].y) * double(a[u].y);
+        er = fma(sg, pr, er);
+      } else {
+        const uint64_t j = i ^ op.xmask;
+        const double ar = a[u].x, ai = a[u].y, br = b[u].x, bi = b[u].y;
+        const double si = (__popcll(i & op.yzmask) & 1) ? -1.0 : 1.0;
+        const double sj = (__popcll(j & op.yzmask) & 1) ? -1.0 : 1.0;
+        // q = B * b ; term_i = conj(a) * q * si
+        const double qr = op.br * br - op.bi * bi, qi = op.br * bi + op.bi * br;
+        er += si * (ar * qr + ai * qi);
+        ei += si * (ar * qi - ai * qr);
+        // q' = B * a ; term_j = conj(b) * q' * sj
+        const double pr = op.br * ar - op.bi * ai, pi = op.br * ai + op.bi * ar;
+        er += sj * (br * pr + bi * pi);
+        ei += sj * (br * pi - bi * pr);
+      }
     }
   }
   const double sr = block_sum<kReduceThreads>(er, sh);
