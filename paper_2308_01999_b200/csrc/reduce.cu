@@ -265,28 +265,33 @@ k_expect_pauli(const V* __restrict__ sv, uint64_t npairs, const __grid_constant_
       a[u] = on ? ldg_s(sv + i) : V{};
       if (h >= 0) b[u] = on ? ldg_s(sv + (i ^ op.xmask)) : V{};
     }
+    // per-batch sums in the state's own precision (fp32 for complex64: no
+    // float->double conversions or fp64 math per element), folded into fp64
+    R br_ = R(0), bi_ = R(0);
+    const R obr = R(op.br), obi = R(op.bi);
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
       const uint64_t i = ii[u];
       if (h < 0) {
-        const double sg = (__popcll(i & op.yzmask) & 1) ? -1.0 : 1.0;
-        const double pr = double(a[u].x) * double(a[u].x) + double(a[u].y) * double(a[u].y);
-        er = fma(sg, pr, er);
+        const R pr = a[u].x * a[u].x + a[u].y * a[u].y;
+        br_ += (__popcll(i & op.yzmask) & 1) ? -pr : pr;
       } else {
         const uint64_t j = i ^ op.xmask;
-        const double ar = a[u].x, ai = a[u].y, br = b[u].x, bi = b[u].y;
-        const double si = (__popcll(i & op.yzmask) & 1) ? -1.0 : 1.0;
-        const double sj = (__popcll(j & op.yzmask) & 1) ? -1.0 : 1.0;
+        const R ar = a[u].x, ai = a[u].y, bre = b[u].x, bim = b[u].y;
+        const R si = (__popcll(i & op.yzmask) & 1) ? R(-1) : R(1);
+        const R sj = (__popcll(j & op.yzmask) & 1) ? R(-1) : R(1);
         // q = B * b ; term_i = conj(a) * q * si
-        const double qr = op.br * br - op.bi * bi, qi = op.br * bi + op.bi * br;
-        er += si * (ar * qr + ai * qi);
-        ei += si * (ar * qi - ai * qr);
+        const R qr = obr * bre - obi * bim, qi = obr * bim + obi * bre;
+        br_ += si * (ar * qr + ai * qi);
+        bi_ += si * (ar * qi - ai * qr);
         // q' = B * a ; term_j = conj(b) * q' * sj
-        const double pr = op.br * ar - op.bi * ai, pi = op.br * ai + op.bi * ar;
-        er += sj * (br * pr + bi * pi);
-        ei += sj * (br * pi - bi * pr);
+        const R pr = obr * ar - obi * ai, pi = obr * ai + obi * ar;
+        br_ += sj * (bre * pr + bim * pi);
+        bi_ += sj * (bre * pi - bim * pr);
       }
     }
+    er += double(br_);
+    ei += double(bi_);
   }
   const double sr = block_sum<kReduceThreads>(er, sh);
   const double si = block_sum<kReduceThreads>(ei, sh);
@@ -296,9 +301,64 @@ k_expect_pauli(const V* __restrict__ sv, uint64_t npairs, const __grid_constant_
   }
 }
 
+// Z-only strings (no bit flip): sum of +-|a_i|^2 over 16-byte units (two
+// complex64 / one complex128 amplitude), per-batch sums in the state's
+// precision folded into fp64.
+template <typename R>
+__global__ void __launch_bounds__(kReduceThreads)
+k_expect_z(const float4* __restrict__ sv, uint64_t nunits, uint64_t yzmask, double* __restrict__ partial) {
+  __shared__ double sh[kReduceThreads / 32];
+  constexpr int APU = sizeof(R) == 4 ? 2 : 1;
+  double er = 0.0;
+  const uint64_t t0 = uint64_t(blockIdx.x) * kChunkUnits + threadIdx.x;
+  constexpr int kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    float4 v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t t = t0 + uint64_t(u0 + u) * kReduceThreads;
+      v[u] = t < nunits ? ldg_s(sv + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    R bs = R(0);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t i = (t0 + uint64_t(u0 + u) * kReduceThreads) * APU;
+      if constexpr (APU == 2) {
+        const float p0 = v[u].x * v[u].x + v[u].y * v[u].y;
+        const float p1 = v[u].z * v[u].z + v[u].w * v[u].w;
+        bs += (__popcll(i & yzmask) & 1) ? -p0 : p0;
+        bs += (__popcll((i + 1) & yzmask) & 1) ? -p1 : p1;
+      } else {
+        const double2 d = *reinterpret_cast<const double2*>(&v[u]);
+        const double pr = d.x * d.x + d.y * d.y;
+        bs += (__popcll(i & yzmask) & 1) ? -pr : pr;
+      }
+    }
+    er += double(bs);
+  }
+  const double sr = block_sum<kReduceThreads>(er, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = sr;
+    partial[2 * blockIdx.x + 1] = 0.0;
+  }
+}
+
 cudaError_t launch_expect_pauli(int dtype, int nbits, const PauliOp& op, const void* sv,
                                 double* d_partial, uint64_t* nchunks_out, cudaStream_t st) {
   const uint64_t n = 1ull << nbits;
+  if (op.hbit < 0 && n >= 2) {
+    const uint64_t nunits = dtype == 1 ? n : n / 2;
+    const uint64_t blocks = chunks_for(nunits);
+    *nchunks_out = blocks;
+    if (dtype == 1)
+      k_expect_z<double><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float4*>(sv), nunits,
+                                                                      op.yzmask, d_partial);
+    else
+      k_expect_z<float><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float4*>(sv), nunits,
+                                                                     op.yzmask, d_partial);
+    return cudaGetLastError();
+  }
   const uint64_t npairs = op.hbit >= 0 ? n / 2 : n;
   const uint64_t blocks = chunks_for(npairs);
   *nchunks_out = blocks;
@@ -312,19 +372,32 @@ cudaError_t launch_expect_pauli(int dtype, int nbits, const PauliOp& op, const v
 }
 
 // ---- <a|b> ----------------------------------------------------------------------------
-template <typename V>
+template <typename V, typename R>
 __global__ void __launch_bounds__(kReduceThreads)
 k_inner(const V* __restrict__ a, const V* __restrict__ b, uint64_t n, double* __restrict__ partial) {
   __shared__ double sh[kReduceThreads / 32];
   double er = 0.0, ei = 0.0;
   const uint64_t t0 = uint64_t(blockIdx.x) * kChunkUnits + threadIdx.x;
-#pragma unroll 4
-  for (int u = 0; u < kReduceUnitsPerThread; ++u) {
-    const uint64_t t = t0 + uint64_t(u) * kReduceThreads;
-    if (t >= n) break;
-    const V x = ldg_s(a + t), y = ldg_s(b + t);
-    er += double(x.x) * double(y.x) + double(x.y) * double(y.y);
-    ei += double(x.x) * double(y.y) - double(x.y) * double(y.x);
+  constexpr int kBatch = 8;
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    V x[kBatch], y[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t t = t0 + uint64_t(u0 + u) * kReduceThreads;
+      const bool on = t < n;
+      x[u] = on ? ldg_s(a + t) : V{};
+      y[u] = on ? ldg_s(b + t) : V{};
+    }
+    // per-batch sums in the vectors' precision, folded into fp64
+    R sr_ = R(0), si_ = R(0);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      sr_ += x[u].x * y[u].x + x[u].y * y[u].y;
+      si_ += x[u].x * y[u].y - x[u].y * y[u].x;
+    }
+    er += double(sr_);
+    ei += double(si_);
   }
   const double sr = block_sum<kReduceThreads>(er, sh);
   const double si = block_sum<kReduceThreads>(ei, sh);
@@ -339,10 +412,10 @@ cudaError_t launch_inner(int dtype, uint64_t namps, const void* a, const void* b
   const uint64_t blocks = chunks_for(namps);
   *nchunks_out = blocks;
   if (dtype == 1)
-    k_inner<double2><<<unsigned(blocks), kReduceThreads, 0, st>>>(
+    k_inner<double2, double><<<unsigned(blocks), kReduceThreads, 0, st>>>(
         static_cast<const double2*>(a), static_cast<const double2*>(b), namps, d_partial);
   else
-    k_inner<float2><<<unsigned(blocks), kReduceThreads, 0, st>>>(
+    k_inner<float2, float><<<unsigned(blocks), kReduceThreads, 0, st>>>(
         static_cast<const float2*>(a), static_cast<const float2*>(b), namps, d_partial);
   return cudaGetLastError();
 }

@@ -411,3 +411,26 @@ def test_native_code_is_what_runs():
     sv.apply(G.cx(3, 7))
     sv.norm_squared()
     assert N.launch_count() - before >= 3
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_expectation_and_inner_kernels(dtype):
+    """Z-only strings (16-byte-unit kernel), strings with X/Y (pair kernel) and
+    <a|b>, all against the oracle / numpy in float64 on the same amplitudes."""
+    rng = np.random.default_rng(11)
+    tol = 1e-5 if dtype == np.complex64 else 1e-12
+    for n in (1, 2, 5, 11, 16):
+        st = random_state(n, rng, dtype)
+        sv = sv_from(st)
+        strings = [((0, "Z"),), ((n - 1, "Z"),), ((0, "X"),), ((n - 1, "Y"),)]
+        if n > 1:
+            strings += [((0, "Z"), (n - 1, "Z")), ((1, "Y"), (0, "Z")), ((0, "X"), (n - 1, "Z"))]
+        for f in strings:
+            coef = 0.5 - 0.25j
+            want = O.expectation_pauli(st.astype(np.complex128), n, f, coef)
+            got = sv.expectation([G.PauliString(f, coef)])
+            assert abs(got - want) < tol * 4, (n, f, got, want)
+        other = random_state(n, rng, dtype)
+        sv2 = sv_from(other)
+        want = np.vdot(st.astype(np.complex128), other.astype(np.complex128))
+        assert abs(sv.native.inner(sv2.native) - want) < tol * 4
