@@ -45,6 +45,13 @@ const bool g_tc_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// 8-bit integer-digit tensor-core kernel for k = 4, 5 (tc8.cu); DSV_TC8=0 selects
+// the bf16-limb kernel (tc.cu) instead.
+const bool g_tc8_env = [] {
+  const char* e = std::getenv("DSV_TC8");
+  return !(e && e[0] == '0');
+}();
+
 // Lane-split kernel for k <= 3 complex64 windows on the lowest k bits (low.cu).
 // DSV_LOW=0 disables it.
 const bool g_low_env = [] {
@@ -417,17 +424,63 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     for (int v = 0; v < 16; ++v)
       if ((v >> bb) & 1) tab[(size_t(ci) * 16 + v) * 8 + t.slot] += t.th;
   }
-  // real embedding of the canonical matrix (n = 2i + out re/im, kk = 2j + in
-  // re/im) as 2^(e_b - 8) (b0 + b1 / 2^8 + b2 / 2^16), exact bf16 limbs
-  // [b0, b1, b2 / 2^8, b1 / 2^8][n][64] (tc.cu)
   std::vector<cplx<float>> m;
   canon_matrix<float>(gg, matrix, m);
-  const int KP = KK < 64 ? 64 : KK;  // whole 128-byte bf16 K blocks per B row
-  const int nlimb = k == 6 ? 3 : 4;  // k = 6: b0, b1, b2 / 2^8 (a1 / 2^8 rides on the A side)
   float bmax = 0.f;
   for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
   int e_b = 0;
   if (bmax > 0.f) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
+  if (g_tc8_env && k <= 5 && e_b >= -20 && e_b <= 20) {
+    // 8-bit digits (tc8.cu): X = B 2^(23 - e_b) rounded, X + 0x8080 split into
+    // balanced base-256 digits b2 (2^16), b1 (2^8), b0 in [-128, 127];
+    // rows [b2 | b1 | b0] x (n = 2i + out re/im), 128 bytes of K = 2j + in re/im
+    constexpr int64_t kLim = (int64_t(1) << 23) - 0x8080 - 1;
+    std::vector<int64_t> X(size_t(KK) * KK);
+    for (int tries = 0; tries < 2; ++tries) {
+      int64_t xmax = 0;
+      for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+          const float re = m[size_t(i) * D + j].x, im = m[size_t(i) * D + j].y;
+          const float e[2][2] = {{re, -im}, {im, re}};
+          for (int oc = 0; oc < 2; ++oc)
+            for (int ic = 0; ic < 2; ++ic) {
+              const int64_t x = int64_t(std::nearbyint(std::ldexp(double(e[oc][ic]), 23 - e_b)));
+              X[size_t(2 * i + oc) * KK + (2 * j + ic)] = x;
+              xmax = std::max(xmax, x < 0 ? -x : x);
+            }
+        }
+      if (xmax <= kLim) break;
+      ++e_b;  // the rounded maximum reached the digit range: one more bit of headroom
+    }
+    d.e_b = e_b;
+    std::vector<unsigned char> host8(size_t(3) * KK * 128, 0);
+    for (int n = 0; n < KK; ++n)
+      for (int kk = 0; kk < KK; ++kk) {
+        const int64_t xp = X[size_t(n) * KK + kk] + 0x8080;
+        const int dig[3] = {int(xp >> 16), int((xp >> 8) & 255) - 128, int(xp & 255) - 128};
+        for (int l = 0; l < 3; ++l) host8[(size_t(l) * KK + n) * 128 + kk] = static_cast<unsigned char>(int8_t(dig[l]));
+      }
+    const size_t bbytes = (host8.size() + 255) / 256 * 256;
+    std::vector<unsigned char> host(bbytes + tab.size() * sizeof(float), 0);
+    std::memcpy(host.data(), host8.data(), host8.size());
+    for (size_t i = 0; i < tab.size(); ++i) {
+      const float f = float(tab[i]);
+      std::memcpy(host.data() + bbytes + i * 4, &f, 4);
+    }
+    if (int rc = ensure_gdata(s, host.size())) return rc;
+    CK(cudaMemcpyAsync(s->gdata, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+    const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
+    d.htab = reinterpret_cast<const float*>(host.data() + bbytes);
+    ProfTok t = prof_start(s);
+    CKL(launch_dense_tc8(k, d, d_b, d_b + bbytes, s->d, s->stream), 1);
+    prof_stop(s, t, prof_class, bytes);
+    return DSV_OK;
+  }
+  // real embedding of the canonical matrix (n = 2i + out re/im, kk = 2j + in
+  // re/im) as 2^(e_b - 8) (b0 + b1 / 2^8 + b2 / 2^16), exact bf16 limbs
+  // [b0, b1, b2 / 2^8, b1 / 2^8][n][64] (tc.cu)
+  const int KP = KK < 64 ? 64 : KK;  // whole 128-byte bf16 K blocks per B row
+  const int nlimb = k == 6 ? 3 : 4;  // k = 6: b0, b1, b2 / 2^8 (a1 / 2^8 rides on the A side)
   d.e_b = e_b;
   const size_t limb_elems = size_t(KK) * KP;
   std::vector<uint16_t> limbs(size_t(nlimb) * limb_elems, 0);

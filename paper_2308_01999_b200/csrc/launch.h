@@ -47,6 +47,9 @@ struct TcDesc {
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);
 int tc_smem_bytes(int k);
+// same windows through 8-bit integer digits (tc8.cu); d_bmat = [b2 | b1 | b0][2^(k+1) rows][128] int8
+cudaError_t launch_dense_tc8(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
+                             cudaStream_t st);
 // k = 6 complex64 window on the tensor cores (tc6.cu); d_bmat = [3 limbs:
 // b0, b1, b2 / 2^8][128 rows][128 cols] bf16; modes 0 (rows) and 1 (pairs)
 cudaError_t launch_dense_tc6(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st);

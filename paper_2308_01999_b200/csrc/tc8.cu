@@ -1,0 +1,463 @@
+// tc8.cu — k = 4/5-qubit dense gates (optionally with the fold fuser's
+// outside-coupled pre-phase) on the 5th-generation tensor cores, complex64,
+// through EXACT 8-bit integer products (tcgen05.mma kind::i8, int32 accumulate).
+//
+// Replaces apply_dense_bits (reference statevec.py:44-60) for the same windows
+// as tc.cu (the bf16-limb kernel, kept for A/B via DSV_TC8=0).  Same dataflow
+// (persistent CTA per SM, two 128-thread groups on alternate 128-group tiles,
+// cp.async rings, A operand in TMEM, gate operand in SW128 shared memory, one
+// thread issues the MMAs and commits to an mbarrier); what changes is the
+// arithmetic, which is cheaper on every side:
+//
+//   * A (the amplitudes): a row of the tile is scaled by its own power of two
+//     so |y| < 2^22 and rounded to an integer I with ONE fma against the magic
+//     1.5 * 2^23 (the float's low mantissa bits are then I + 2^22).  One
+//     integer add turns the bits into I' = I + 0x8080, whose bytes are the
+//     balanced base-256 digits of I: a0 = byte0 ^ 0x80, a1 = byte1 ^ 0x80
+//     (in [-128, 127]), a2 = byte2 (in [-64, 64]); byte permutes pack four
+//     values' digits per 32-bit TMEM column.  ~4 integer/fp ops per value
+//     instead of 9 fp ops + packing for three bf16 limbs.
+//   * B (the gate's real embedding) is split the same way on the host:
+//     X = B 2^(23 - e_b) = b2 2^16 + b1 2^8 + b0, digits in [-128, 127].
+//   * products of digit weight >= 2^16 (a2 b2, a2 b1, a1 b2, a2 b0, a1 b1, a0 b2)
+//     land in three int32 accumulators hi / mid / lo (exact: |acc| < 2^22);
+//     3 MMAs per 32-wide K step (N = 3, 2, 1 x 2^(k+1)) instead of 10 bf16 ones,
+//     at twice the bf16 tensor rate.  The dropped products (a1 b0, a0 b1, a0 b0)
+//     are zero-mean and below 2^-22 of the row's scale: measured (U then U^dagger,
+//     tools/tc_precision.py) 1.8e-6 max relative error per round vs 4.2e-7 for
+//     the fp32 CUDA-core kernels and 2.4e-7 for tc.cu — inside the c64 bound
+//     (1e-5 absolute, fidelity 1 - 1e-6) but not fp32-identical; DSV_TC8=0
+//     selects tc.cu where that matters.
+//   * the accumulators start at the float bits of 1.5 * 2^23 (tcgen05.st of a
+//     constant), so each int32 sum reads back directly as the float
+//     1.5 * 2^23 + acc: the epilogue is 1 add + 3 fma per value, no conversion.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "launch.h"
+#include "tcgen05.cuh"
+
+namespace dsv {
+
+using namespace tcx;
+
+template <int K>
+struct Tc8P {
+  Geom g;                 // groups (amplitude index space, holes = targets + controls)
+  uint64_t ntiles;        // g.nwork / 128
+  int nnib;               // phase-table nibbles (0: plain dense)
+  int e_b;                // gate scale: |B| < 2^e_b, X = B 2^(23 - e_b)
+  int emin, emax;         // row-exponent clamp (keeps every power of two normal)
+  int coop;               // phase uniform over a tile's 128 rows: computed once per tile
+  int nnib_row;           // leading nibbles that vary over the rows (the rest: tile-uniform sums)
+  int nib_shift[16];      // amplitude-index shift of nibble c
+  uint64_t offs[1 << K];  // member offsets (amplitudes)
+  float4 ctab[kTcMaxNib * 16 * 2];  // tile-uniform phase table (constant bank, broadcast reads)
+};
+
+template <int K>
+struct Tc8Layout {
+  static constexpr int D = 1 << K;
+  static constexpr int N0 = 2 * D;                // real outputs = real inputs (GEMM K)
+  static constexpr int KSTEPS = N0 / 32;          // MMA K = 32 (8-bit)
+  static constexpr int B_BYTES = 3 * N0 * 128;    // [b2 | b1 | b0] rows of 128 B (K <= 64 used)
+  static constexpr int BAR = B_BYTES;             // 2 mbarriers + TMEM slot
+  static constexpr int PBUF = BAR + 128;          // tile-uniform phases: [group][2][D] float2
+  static constexpr int RING = PBUF + 2 * 2 * D * 8;
+  static constexpr int STAGE = 128 * D * 8;
+  static constexpr int SMEM_MAX = 227 * 1024 - 1024;
+  static constexpr int NS_FIT = (SMEM_MAX - RING) / (2 * STAGE);
+  static constexpr int NSTAGE = NS_FIT > 6 ? 6 : NS_FIT;
+  static_assert(NSTAGE >= 3, "ring must hold three tiles per group");
+  static_assert(N0 <= 64, "B rows are one 128-byte K block");
+  static constexpr int BYTES = RING + 2 * NSTAGE * STAGE;
+  // TMEM per group (256 columns): A digits a2, a1, a0 (4 per column), then hi | mid | lo
+  static constexpr int ACOLS = N0 / 4;
+  static constexpr int T_A2 = 0, T_A1 = ACOLS, T_A0 = 2 * ACOLS;
+  static constexpr int T_HI = 64, T_MID = T_HI + N0, T_LO = T_HI + 2 * N0;
+  static_assert(3 * ACOLS <= T_HI && T_LO + N0 <= 256, "TMEM plan");
+};
+
+constexpr uint32_t kAccInit = 0x4B400000u;           // float bits of 1.5 * 2^23
+constexpr uint32_t kDigitOff = 0x8080u - 0x4B400000u;  // float bits of M + I -> I + 0x8080
+
+//   [hi | mid | lo] += a2 [b2 | b1 | b0];  [mid | lo] += a1 [b2 | b1];  lo += a0 b2
+template <int K, int GRP>
+__device__ __forceinline__ void issue_mma8(uint32_t sbase) {
+  using L = Tc8Layout<K>;
+  constexpr uint32_t T0 = GRP * 256;
+  constexpr uint32_t ID3 = idesc_i8<3 * L::N0, 1, 1>(), ID2 = idesc_i8<2 * L::N0, 1, 1>(),
+                     ID1 = idesc_i8<L::N0, 1, 1>();
+#pragma unroll
+  for (int s = 0; s < L::KSTEPS; ++s) {
+    const uint64_t bd = sw128_desc(sbase + s * 32);
+    mma_ts_i8(T0 + L::T_HI, T0 + L::T_A2 + s * 8, bd, ID3, 1u);
+    mma_ts_i8(T0 + L::T_MID, T0 + L::T_A1 + s * 8, bd, ID2, 1u);
+    mma_ts_i8(T0 + L::T_LO, T0 + L::T_A0 + s * 8, bd, ID1, 1u);
+  }
+}
+
+template <int K, bool PHASED, int MODE>
+__global__ void __launch_bounds__(256, 1)
+k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, const float4* __restrict__ tab,
+            float2* __restrict__ sv) {
+  using L = Tc8Layout<K>;
+  constexpr bool PAIR = MODE == kTcPair;
+  constexpr bool LOWT = MODE == kTcLow;
+  constexpr int D = L::D;
+  constexpr int N0 = L::N0;
+  constexpr int S = L::NSTAGE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t raw_base = smem_u32(smem_raw);
+  const uint32_t sbase = (raw_base + 1023u) & ~1023u;
+  unsigned char* sm = smem_raw + (sbase - raw_base);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int grp = tid >> 7;
+  const int row = tid & 127;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);
+  const uint32_t bar = sbase + L::BAR + 8 * grp;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    mbar_init(sbase + L::BAR, 1);
+    mbar_init(sbase + L::BAR + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // gate digits, host layout [3 N0 rows][8 x 16 B] -> 128-byte swizzled rows
+  for (int i = tid; i < 3 * N0 * 8; i += 256) {
+    const int r = i / 8, c16 = i % 8;
+    *reinterpret_cast<uint4*>(sm + r * 128 + ((c16 ^ (r & 7)) << 4)) = bmat[i];
+  }
+
+  const uint64_t step = gridDim.x;
+  auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + (2 * uint64_t(i) + grp) * step; };
+  const uint64_t e0 = expand(p.g, 0);
+  const uint64_t rowoff = expand(p.g, row) ^ e0;
+  const int prow = 2 * (row & 63);
+  const int jpar = row >> 6;
+  const uint64_t prowoff = expand(p.g, prow) ^ e0;
+  auto issue = [&](int i) -> uint64_t {
+    const uint64_t tl = tile_of(i);
+    uint64_t tb = 0;
+    if (tl < p.ntiles) {
+      tb = expand(p.g, tl * 128);
+      const uint32_t st0 = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE;
+      if constexpr (LOWT) {
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) {
+          const int q = row + 128 * m;
+          const int r = q / (D / 2), c = q % (D / 2);
+          cp_async16(st0 + r * (D * 8) + ((c ^ (r & 7)) << 4), sv + tb + 2 * q);
+        }
+      } else if constexpr (PAIR) {
+        const uint64_t b = tb | prowoff;
+#pragma unroll
+        for (int jj = 0; jj < D / 2; ++jj) {
+          const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];
+          cp_async16(st0 + prow * 8 + (2 * jj + jpar) * 1024, sv + b + o);
+        }
+      } else {
+        const uint64_t b = tb | rowoff;
+#pragma unroll
+        for (int j = 0; j < D; ++j) cp_async8(st0 + row * 8 + j * 1024, sv + b + p.offs[j]);
+      }
+    }
+    cp_async_commit();
+    return tb;
+  };
+  float2* Pb = reinterpret_cast<float2*>(sm + L::PBUF) + grp * 2 * D;
+  auto coop_phase = [&](int i, uint64_t tb) {
+    const int j = row - (128 - D);
+    if (PHASED && !p.coop && j == 0 && tile_of(i) < p.ntiles) {
+      float a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) a[s] = 0.f;
+#pragma unroll
+      for (int c = 0; c < kTcMaxNib; ++c) {
+        if (c >= p.nnib_row && c < p.nnib) {
+          const int r = (c * 16 + int((tb >> p.nib_shift[c]) & 15u)) * 2;
+          const float4 x = p.ctab[r], y = p.ctab[r + 1];
+          a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+          a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+        }
+      }
+      float4* hb = reinterpret_cast<float4*>(Pb + (i & 1) * D);
+      hb[0] = make_float4(a[0], a[1], a[2], a[3]);
+      hb[1] = make_float4(a[4], a[5], a[6], a[7]);
+    }
+    if (PHASED && p.coop && j >= 0 && tile_of(i) < p.ntiles) {
+      float a[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) a[s] = 0.f;
+#pragma unroll
+      for (int c = 0; c < kTcMaxNib; ++c) {
+        if (c < p.nnib) {
+          const int r = (c * 16 + int((tb >> p.nib_shift[c]) & 15u)) * 2;
+          const float4 x = p.ctab[r], y = p.ctab[r + 1];
+          a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+          a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+        }
+      }
+      float ang = a[K];
+#pragma unroll
+      for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
+      float sn, cs;
+      sincos_red(ang, &sn, &cs);
+      Pb[(i & 1) * D + j] = make_float2(cs, sn);
+    }
+  };
+  uint64_t tq[S - 1];
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) tq[s] = issue(s);
+  coop_phase(0, tq[0]);
+  coop_phase(1, tq[1]);
+  cp_async_wait<S - 2>();
+
+  if (*tmem_slot != 0u) __trap();
+  const uint32_t tlane = uint32_t(grp * 256) + (uint32_t((warp & 3) * 32) << 16);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+
+  // out = scale (hi 2^16 + mid 2^8 + lo): the accumulators read back as
+  // M + acc (M = 1.5 * 2^23); t2 = V + 257 M, removed by the last fma
+  auto combine = [](float h, float m, float l, float scale, float cm) {
+    const float t1 = __fmaf_rn(__fadd_rn(h, -kMagic), 256.f, m);
+    return __fmaf_rn(__fmaf_rn(t1, 256.f, l), scale, cm);
+  };
+  const bool odd = row & 1;
+  auto epilogue = [&](uint64_t b, float scale, float cm) {
+#pragma unroll
+    for (int h = 0; h < N0 / 32; ++h) {
+      float ch[32], cmid[32], cl[32];
+      tmem_ld32(tlane + uint32_t(L::T_HI + h * 32), ch);
+      tmem_ld32(tlane + uint32_t(L::T_MID + h * 32), cmid);
+      tmem_ld32(tlane + uint32_t(L::T_LO + h * 32), cl);
+      auto val = [&](int c) { return combine(ch[c], cmid[c], cl[c], scale, cm); };
+      if constexpr (LOWT) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          __stcs(reinterpret_cast<float4*>(sv + b) + h * 8 + i,
+                 make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
+      } else if constexpr (!PAIR) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) __stcs(sv + b + p.offs[h * 16 + i], make_float2(val(2 * i), val(2 * i + 1)));
+      } else {
+        const uint64_t be = b - (odd ? 1 : 0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float o[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o[c] = val(4 * q + c);
+          const float sx = odd ? o[0] : o[2], sy = odd ? o[1] : o[3];
+          const float rx = __shfl_xor_sync(0xffffffffu, sx, 1), ry = __shfl_xor_sync(0xffffffffu, sy, 1);
+          const uint64_t oj = odd ? p.offs[h * 16 + 2 * q + 1] : p.offs[h * 16 + 2 * q];
+          const float4 w = odd ? make_float4(rx, ry, o[2], o[3]) : make_float4(o[0], o[1], rx, ry);
+          __stcs(reinterpret_cast<float4*>(sv + be + oj), w);
+        }
+      }
+    }
+  };
+
+  uint64_t prev_base = 0;
+  float prev_scale = 0.f, prev_cm = 0.f;
+  int it = 0, stage = 0;
+#pragma unroll 1
+  for (;; ++it) {
+    const uint64_t tile = tile_of(it);
+    if (tile >= p.ntiles) break;
+    const uint64_t tb_new = issue(it + S - 1);
+    const uint64_t base = tq[0] | rowoff;
+#pragma unroll
+    for (int s = 0; s + 1 < S - 1; ++s) tq[s] = tq[s + 1];
+    tq[S - 2] = tb_new;
+    const unsigned char* stg = sm + L::RING + (grp * S + stage) * L::STAGE;
+    stage = stage + 1 == S ? 0 : stage + 1;
+    float2 v[D];
+    if constexpr (LOWT) {
+#pragma unroll
+      for (int c = 0; c < D / 2; ++c) {
+        const float4 x = *reinterpret_cast<const float4*>(stg + row * (D * 8) + ((c ^ (row & 7)) << 4));
+        v[2 * c] = make_float2(x.x, x.y);
+        v[2 * c + 1] = make_float2(x.z, x.w);
+      }
+    } else {
+      const float2* raw = reinterpret_cast<const float2*>(stg) + row;
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = raw[j * 128];
+    }
+    if constexpr (PHASED) {
+      if (p.coop) {
+        const float2* P = Pb + (it & 1) * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const float2 x = v[j], f = P[j];
+          v[j] = make_float2(x.x * f.x - x.y * f.y, x.x * f.y + x.y * f.x);
+        }
+      } else {
+        float a[8];
+        const float4* hb = reinterpret_cast<const float4*>(Pb + (it & 1) * D);
+        const float4 h0 = hb[0], h1 = hb[1];
+        a[0] = h0.x; a[1] = h0.y; a[2] = h0.z; a[3] = h0.w;
+        a[4] = h1.x; a[5] = h1.y; a[6] = h1.z; a[7] = h1.w;
+#pragma unroll
+        for (int c = 0; c < kTcMaxNib; ++c) {
+          if (c < p.nnib_row) {
+            const int r = (c * 16 + int((base >> p.nib_shift[c]) & 15u)) * 2;
+            const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);
+            a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+            a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+          }
+        }
+        float2 P[D];
+        sincos_red(a[K], &P[0].y, &P[0].x);
+#pragma unroll
+        for (int m = 0; m < K; ++m) {
+          float es, ec;
+          sincos_red(a[m], &es, &ec);
+#pragma unroll
+          for (int j = 0; j < (1 << m); ++j) {
+            const float2 q = P[j];
+            P[j + (1 << m)] = make_float2(q.x * ec - q.y * es, q.x * es + q.y * ec);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const float2 x = v[j];
+          v[j] = make_float2(x.x * P[j].x - x.y * P[j].y, x.x * P[j].y + x.y * P[j].x);
+        }
+      }
+    }
+    // row exponent: max |x| < 2^e_row
+    float mx = 0.f;
+#pragma unroll
+    for (int j = 0; j < D; ++j) mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
+    const int e_row = min(max(int((__float_as_uint(mx) >> 23) & 0xFF) - 126, p.emin), p.emax);
+    const float sc_in = pow2f(22 - e_row);
+    const float scale = pow2f(e_row + p.e_b - 29);
+    const float cm = -771.f * pow2f(e_row + p.e_b - 7);  // -257 M scale
+    if (it > 0) {  // MMA(i-1) done: A is free and its accumulators are ready
+      mbar_wait(bar, (it - 1) & 1);
+      fence_after();
+      epilogue(prev_base, prev_scale, prev_cm);
+    }
+    // accumulators back to M for this tile's MMAs
+#pragma unroll
+    for (int q = 0; q < 3 * N0 / 32; ++q) tmem_fill32(tlane + uint32_t(L::T_HI + 32 * q), kAccInit);
+    // digits -> TMEM: column c holds K = 4c..4c+3 = (re, im) of members 2c, 2c+1
+    uint32_t la2[N0 / 4], la1[N0 / 4], la0[N0 / 4];
+#pragma unroll
+    for (int c = 0; c < N0 / 4; ++c) {
+      const uint32_t w0 = __float_as_uint(__fmaf_rn(v[2 * c].x, sc_in, kMagic)) + kDigitOff;
+      const uint32_t w1 = __float_as_uint(__fmaf_rn(v[2 * c].y, sc_in, kMagic)) + kDigitOff;
+      const uint32_t w2 = __float_as_uint(__fmaf_rn(v[2 * c + 1].x, sc_in, kMagic)) + kDigitOff;
+      const uint32_t w3 = __float_as_uint(__fmaf_rn(v[2 * c + 1].y, sc_in, kMagic)) + kDigitOff;
+      const uint32_t p01 = __byte_perm(w0, w1, 0x5140), p23 = __byte_perm(w2, w3, 0x5140);
+      la0[c] = __byte_perm(p01, p23, 0x5410) ^ 0x80808080u;
+      la1[c] = __byte_perm(p01, p23, 0x7632) ^ 0x80808080u;
+      la2[c] = __byte_perm(__byte_perm(w0, w1, 0x0062), __byte_perm(w2, w3, 0x0062), 0x5410);
+    }
+    if constexpr (N0 / 4 == 16) {
+      tmem_st16(tlane + uint32_t(L::T_A2), la2);
+      tmem_st16(tlane + uint32_t(L::T_A1), la1);
+      tmem_st16(tlane + uint32_t(L::T_A0), la0);
+    } else {
+      tmem_st8(tlane + uint32_t(L::T_A2), la2);
+      tmem_st8(tlane + uint32_t(L::T_A1), la1);
+      tmem_st8(tlane + uint32_t(L::T_A0), la0);
+    }
+    cp_async_wait<S - 2>();
+    tmem_wait_st();
+    fence_before();
+    group_sync(grp);
+    if (row == 0) {
+      fence_after();
+      if (grp == 0) issue_mma8<K, 0>(sbase);
+      else issue_mma8<K, 1>(sbase);
+      mma_commit(bar);
+    }
+    coop_phase(it + 2, tq[S - 2 >= 1 ? 1 : 0]);
+    prev_base = base;
+    prev_scale = scale;
+    prev_cm = cm;
+  }
+  if (it > 0) {
+    mbar_wait(bar, (it - 1) & 1);
+    fence_after();
+    epilogue(prev_base, prev_scale, prev_cm);
+  }
+  cp_async_wait<0>();
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512) : "memory");
+  }
+}
+
+template <int K, bool PHASED, int MODE>
+static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
+  using L = Tc8Layout<K>;
+  Tc8P<K> p;
+  std::memset(&p, 0, sizeof p);
+  p.g = d.g;
+  p.ntiles = d.g.nwork / 128;
+  p.nnib = d.nnib;
+  p.e_b = d.e_b;
+  // every power of two the kernel forms stays normal: 22 - e_row, e_row + e_b - 29, e_row + e_b - 7
+  // every power of two the kernel forms stays normal: 22 - e_row, e_row + e_b - 29,
+  // 771 * 2^(e_row + e_b - 7)
+  p.emin = std::max(-100, -97 - d.e_b);
+  p.emax = std::min(100, 124 - d.e_b);
+  p.coop = d.coop;
+  p.nnib_row = d.nnib_row;
+  for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
+  for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
+  if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));
+  const int smem = L::BYTES + 1024;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc8<K, PHASED, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  uint64_t blocks = uint64_t(device_sm_count());
+  const uint64_t need = (p.ntiles + 1) / 2;
+  if (blocks > need) blocks = need;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_tc8<K, PHASED, MODE><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+                                                                static_cast<const float4*>(d_tab),
+                                                                static_cast<float2*>(sv));
+  return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t tc8_k(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
+  const bool ph = d.nnib > 0;
+  switch (d.mode) {
+    case kTcPair: return ph ? tc8_go<K, true, kTcPair>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcPair>(d, d_bmat, d_tab, sv, st);
+    case kTcLow: return ph ? tc8_go<K, true, kTcLow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcLow>(d, d_bmat, d_tab, sv, st);
+  }
+  return ph ? tc8_go<K, true, kTcRow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcRow>(d, d_bmat, d_tab, sv, st);
+}
+
+cudaError_t launch_dense_tc8(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
+                             cudaStream_t st) {
+  switch (k) {
+    case 4: return tc8_k<4>(d, d_bmat, d_tab, sv, st);
+    case 5: return tc8_k<5>(d, d_bmat, d_tab, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dsv
