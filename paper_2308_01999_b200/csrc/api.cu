@@ -221,13 +221,16 @@ int make_geom(int ubits, const std::vector<int>& holes_sorted, uint64_t set_mask
   std::memset(g, 0, sizeof(Geom));
   g->nwork = 1ull << (ubits - H);
   g->set_mask = set_mask;
-  g->nseg = H + 1;
+  g->nseg = 0;
   for (int i = 0; i <= H; ++i) {
     const int lo = i == 0 ? 0 : holes_sorted[i - 1] + 1;
     const int hi = i == H ? 64 : holes_sorted[i];
     uint64_t m = 0;
     for (int b = lo; b < hi; ++b) m |= 1ull << b;
-    g->seg[i] = m;
+    if (m == 0) continue;  // adjacent holes: empty run
+    g->seg[g->nseg] = m;
+    g->shift[g->nseg] = uint8_t(i);
+    ++g->nseg;
   }
   return DSV_OK;
 }
@@ -387,6 +390,9 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   d.g = uv.g;
   d.mode = tc_mode(gg);
   for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
+  d.tshift = gg.tsorted[0];
+  for (int m = 1; m < k; ++m)
+    if (gg.tsorted[m] != gg.tsorted[0] + m) d.tshift = -1;
   // tile rows = the lowest 7 free (non-hole) index bits
   uint64_t row_mask = 0;
   {

@@ -22,15 +22,18 @@ namespace dsv {
 struct Geom {
   uint64_t nwork;     // number of work items
   uint64_t set_mask;  // bits forced to 1 (controls with value 1), in unit index space
-  int nseg;           // holes + 1
+  int nseg;           // non-empty runs of free bits (<= holes + 1)
   int pad_;
-  uint64_t seg[DSV_MAX_GEOM_SEGS];  // seg[i]: output bits that take (w << i)
+  uint64_t seg[DSV_MAX_GEOM_SEGS];     // seg[i]: output bits that take (w << shift[i])
+  uint8_t shift[DSV_MAX_GEOM_SEGS];    // holes below run i
 };
 
-// pdep-style expansion: bits of w between holes i-1 and i are shifted left by i.
+// pdep-style expansion: the bits of w in free run i move up by the number of
+// holes below the run (adjacent holes share one run boundary, so a window of
+// contiguous targets costs two runs, not k + 1).
 __device__ __forceinline__ uint64_t expand(const Geom& g, uint64_t w) {
   uint64_t r = g.set_mask;
-  for (int i = 0; i < g.nseg; ++i) r |= (w << i) & g.seg[i];
+  for (int i = 0; i < g.nseg; ++i) r |= (w << g.shift[i]) & g.seg[i];
   return r;
 }
 

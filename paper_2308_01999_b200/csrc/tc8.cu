@@ -42,6 +42,9 @@ namespace dsv {
 
 using namespace tcx;
 
+#ifndef DSV_TC8_FILL
+#define DSV_TC8_FILL 0  // accumulator start value: 0 per-thread tcgen05.st, 1/2 tcgen05.cp (diagnostics)
+#endif
 template <int K>
 struct Tc8P {
   Geom g;                 // groups (amplitude index space, holes = targets + controls)
@@ -52,6 +55,7 @@ struct Tc8P {
   int coop;               // phase uniform over a tile's 128 rows: computed once per tile
   int nnib_row;           // leading nibbles that vary over the rows (the rest: tile-uniform sums)
   int nib_shift[16];      // amplitude-index shift of nibble c
+  int tshift;             // member j at offset j << tshift (contiguous targets), else -1: offs[]
   uint64_t offs[1 << K];  // member offsets (amplitudes)
   float4 ctab[kTcMaxNib * 16 * 2];  // tile-uniform phase table (constant bank, broadcast reads)
 };
@@ -63,7 +67,8 @@ struct Tc8Layout {
   static constexpr int KSTEPS = N0 / 32;          // MMA K = 32 (8-bit)
   static constexpr int B_BYTES = 3 * N0 * 128;    // [b2 | b1 | b0] rows of 128 B (K <= 64 used)
   static constexpr int BAR = B_BYTES;             // 2 mbarriers + TMEM slot
-  static constexpr int PBUF = BAR + 128;          // tile-uniform phases: [group][2][D] float2
+  static constexpr int MAG = BAR + 128;           // 128 x 32 B of the accumulator start value (tcgen05.cp source)
+  static constexpr int PBUF = MAG + (DSV_TC8_FILL ? 4096 : 0);  // tile-uniform phases: [group][2][D] float2
   static constexpr int RING = PBUF + 2 * 2 * D * 8;
   static constexpr int STAGE = 128 * D * 8;
   static constexpr int SMEM_MAX = 227 * 1024 - 1024;
@@ -135,6 +140,8 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
     const int r = i / 8, c16 = i % 8;
     *reinterpret_cast<uint4*>(sm + r * 128 + ((c16 ^ (r & 7)) << 4)) = bmat[i];
   }
+  if (DSV_TC8_FILL)
+    for (int i = tid; i < 1024; i += 256) reinterpret_cast<uint32_t*>(sm + L::MAG)[i] = kAccInit;
 
   const uint64_t step = gridDim.x;
   auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + (2 * uint64_t(i) + grp) * step; };
@@ -158,15 +165,29 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
         }
       } else if constexpr (PAIR) {
         const uint64_t b = tb | prowoff;
+        if (p.tshift >= 0) {  // member j at j << tshift: one strided pointer
+          const float2* src = sv + b + (uint64_t(jpar) << p.tshift);
+          const uint64_t stride = uint64_t(2) << p.tshift;
 #pragma unroll
-        for (int jj = 0; jj < D / 2; ++jj) {
-          const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];
-          cp_async16(st0 + prow * 8 + (2 * jj + jpar) * 1024, sv + b + o);
+          for (int jj = 0; jj < D / 2; ++jj) cp_async16(st0 + prow * 8 + (2 * jj + jpar) * 1024, src + jj * stride);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < D / 2; ++jj) {
+            const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];
+            cp_async16(st0 + prow * 8 + (2 * jj + jpar) * 1024, sv + b + o);
+          }
         }
       } else {
         const uint64_t b = tb | rowoff;
+        if (p.tshift >= 0) {
+          const float2* src = sv + b;
+          const uint64_t stride = uint64_t(1) << p.tshift;
 #pragma unroll
-        for (int j = 0; j < D; ++j) cp_async8(st0 + row * 8 + j * 1024, sv + b + p.offs[j]);
+          for (int j = 0; j < D; ++j) cp_async8(st0 + row * 8 + j * 1024, src + j * stride);
+        } else {
+#pragma unroll
+          for (int j = 0; j < D; ++j) cp_async8(st0 + row * 8 + j * 1024, sv + b + p.offs[j]);
+        }
       }
     }
     cp_async_commit();
@@ -248,10 +269,20 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
           __stcs(reinterpret_cast<float4*>(sv + b) + h * 8 + i,
                  make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
       } else if constexpr (!PAIR) {
+        if (p.tshift >= 0) {
+          float2* dst = sv + b + (uint64_t(h * 16) << p.tshift);
+          const uint64_t stride = uint64_t(1) << p.tshift;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) __stcs(sv + b + p.offs[h * 16 + i], make_float2(val(2 * i), val(2 * i + 1)));
+          for (int i = 0; i < 16; ++i) __stcs(dst + i * stride, make_float2(val(2 * i), val(2 * i + 1)));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) __stcs(sv + b + p.offs[h * 16 + i], make_float2(val(2 * i), val(2 * i + 1)));
+        }
       } else {
         const uint64_t be = b - (odd ? 1 : 0);
+        // even lane: member 2q of both rows, odd lane: member 2q + 1
+        float2* dst = sv + be + (p.tshift >= 0 ? (uint64_t(h * 16 + (odd ? 1 : 0)) << p.tshift) : 0);
+        const uint64_t stride = p.tshift >= 0 ? (uint64_t(2) << p.tshift) : 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float o[4];
@@ -259,9 +290,13 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
           for (int c = 0; c < 4; ++c) o[c] = val(4 * q + c);
           const float sx = odd ? o[0] : o[2], sy = odd ? o[1] : o[3];
           const float rx = __shfl_xor_sync(0xffffffffu, sx, 1), ry = __shfl_xor_sync(0xffffffffu, sy, 1);
-          const uint64_t oj = odd ? p.offs[h * 16 + 2 * q + 1] : p.offs[h * 16 + 2 * q];
           const float4 w = odd ? make_float4(rx, ry, o[2], o[3]) : make_float4(o[0], o[1], rx, ry);
-          __stcs(reinterpret_cast<float4*>(sv + be + oj), w);
+          if (p.tshift >= 0) {
+            __stcs(reinterpret_cast<float4*>(dst + q * stride), w);
+          } else {
+            const uint64_t oj = odd ? p.offs[h * 16 + 2 * q + 1] : p.offs[h * 16 + 2 * q];
+            __stcs(reinterpret_cast<float4*>(sv + be + oj), w);
+          }
         }
       }
     }
@@ -349,9 +384,11 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
       fence_after();
       epilogue(prev_base, prev_scale, prev_cm);
     }
+#if DSV_TC8_FILL == 0
     // accumulators back to M for this tile's MMAs
 #pragma unroll
     for (int q = 0; q < 3 * N0 / 32; ++q) tmem_fill32(tlane + uint32_t(L::T_HI + 32 * q), kAccInit);
+#endif
     // digits -> TMEM: column c holds K = 4c..4c+3 = (re, im) of members 2c, 2c+1
     uint32_t la2[N0 / 4], la1[N0 / 4], la0[N0 / 4];
 #pragma unroll
@@ -380,6 +417,16 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
     group_sync(grp);
     if (row == 0) {
       fence_after();
+#if DSV_TC8_FILL == 1
+      // accumulators back to M (tcgen05.cp of a constant block, ordered before the MMAs)
+      const uint64_t md = plain_desc(sbase + L::MAG, 128, 128);
+#pragma unroll
+      for (int q = 0; q < 3 * N0 / 4; ++q) tmem_cp_x4(uint32_t(grp * 256 + L::T_HI + 4 * q), md);
+#elif DSV_TC8_FILL == 2
+      const uint64_t md = plain_desc(sbase + L::MAG, 128, 256);
+#pragma unroll
+      for (int q = 0; q < 3 * N0 / 8; ++q) tmem_cp_128x256(uint32_t(grp * 256 + L::T_HI + 8 * q), md);
+#endif
       if (grp == 0) issue_mma8<K, 0>(sbase);
       else issue_mma8<K, 1>(sbase);
       mma_commit(bar);
@@ -419,6 +466,10 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
   p.emax = std::min(100, 124 - d.e_b);
   p.coop = d.coop;
   p.nnib_row = d.nnib_row;
+  p.tshift = d.tshift;
+#ifdef DSV_TC8_NOSTRIDE
+  p.tshift = -1;
+#endif
   for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
   if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));

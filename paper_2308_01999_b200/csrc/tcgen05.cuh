@@ -62,6 +62,23 @@ __device__ __forceinline__ void mma_ss_i8(uint32_t tmem_d, uint64_t ad, uint64_t
       "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate));
 }
 
+// shared-memory matrix descriptor without swizzle (canonical 8-row x 16-byte core matrices)
+__device__ __forceinline__ uint64_t plain_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (uint64_t(1) << 46);
+}
+
+// 32 rows x 128 bits of shared memory -> 4 TMEM columns of all 128 lanes
+// (multicast to the four lane quarters); async, ordered with later tcgen05.mma
+__device__ __forceinline__ void tmem_cp_x4(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
+// 128 rows x 256 bits of shared memory -> 8 TMEM columns of 128 lanes
+__device__ __forceinline__ void tmem_cp_128x256(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
