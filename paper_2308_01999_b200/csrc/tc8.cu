@@ -130,6 +130,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  if (tid < 2) reinterpret_cast<uint32_t*>(sm + L::BAR + 32)[tid] = kAccInit;
   if (tid == 32) {
     mbar_init(sbase + L::BAR, 1);
     mbar_init(sbase + L::BAR + 8, 1);
@@ -239,6 +240,24 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
   for (int s = 0; s < S - 1; ++s) tq[s] = issue(s);
   coop_phase(0, tq[0]);
   coop_phase(1, tq[1]);
+  // per-row phase slots (row-varying nibbles) of this thread's row in the
+  // NEXT tile, loaded one iteration ahead so the table latency stays off the
+  // critical path
+  float ra[8];
+  auto row_angles = [&](uint64_t b) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) ra[s] = 0.f;
+#pragma unroll
+    for (int c = 0; c < kTcMaxNib; ++c) {
+      if (c < p.nnib_row) {
+        const int r = (c * 16 + int((b >> p.nib_shift[c]) & 15u)) * 2;
+        const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);
+        ra[0] += x.x; ra[1] += x.y; ra[2] += x.z; ra[3] += x.w;
+        ra[4] += y.x; ra[5] += y.y; ra[6] += y.z; ra[7] += y.w;
+      }
+    }
+  };
+  if (PHASED && !p.coop) row_angles(tq[0] | rowoff);
   cp_async_wait<S - 2>();
 
   if (*tmem_slot != 0u) __trap();
@@ -254,7 +273,6 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
     const float t1 = __fmaf_rn(__fadd_rn(h, -kMagic), 256.f, m);
     return __fmaf_rn(__fmaf_rn(t1, 256.f, l), scale, cm);
   };
-  const bool odd = row & 1;
   auto epilogue = [&](uint64_t b, float scale, float cm) {
 #pragma unroll
     for (int h = 0; h < N0 / 32; ++h) {
@@ -268,19 +286,11 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
         for (int i = 0; i < 8; ++i)
           __stcs(reinterpret_cast<float4*>(sv + b) + h * 8 + i,
                  make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
-      } else if constexpr (!PAIR) {
-        if (p.tshift >= 0) {
-          float2* dst = sv + b + (uint64_t(h * 16) << p.tshift);
-          const uint64_t stride = uint64_t(1) << p.tshift;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) __stcs(dst + i * stride, make_float2(val(2 * i), val(2 * i + 1)));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) __stcs(sv + b + p.offs[h * 16 + i], make_float2(val(2 * i), val(2 * i + 1)));
-        }
-      } else {
+      } else if constexpr (PAIR && !PHASED) {
+        // lanes 2t', 2t'+1 hold adjacent amplitudes: swap one member per pair
+        // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1)
+        const bool odd = row & 1;
         const uint64_t be = b - (odd ? 1 : 0);
-        // even lane: member 2q of both rows, odd lane: member 2q + 1
         float2* dst = sv + be + (p.tshift >= 0 ? (uint64_t(h * 16 + (odd ? 1 : 0)) << p.tshift) : 0);
         const uint64_t stride = p.tshift >= 0 ? (uint64_t(2) << p.tshift) : 0;
 #pragma unroll
@@ -298,10 +308,33 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
             __stcs(reinterpret_cast<float4*>(sv + be + oj), w);
           }
         }
+      } else {
+        // 8-byte stores of this row's members: with index bit 0 free (PAIR)
+        // adjacent lanes hold adjacent amplitudes, so each warp store is one
+        // contiguous 256-byte run without any lane exchange (measured faster
+        // than the 16-byte pair exchange for the phased windows, slower for
+        // plain ones)
+        if (p.tshift >= 0) {
+          float2* dst = sv + b + (uint64_t(h * 16) << p.tshift);
+          const uint64_t stride = uint64_t(1) << p.tshift;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __stcs(dst, make_float2(val(2 * i), val(2 * i + 1)));
+            dst += stride;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) __stcs(sv + b + p.offs[h * 16 + i], make_float2(val(2 * i), val(2 * i + 1)));
+        }
       }
     }
   };
 
+  // (loaded from shared memory so the compiler keeps them in registers rather
+  // than re-materialising eight immediates for every store)
+  uint32_t mg[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mg[i] = reinterpret_cast<const uint32_t*>(sm + L::BAR + 32)[i & 1];
   uint64_t prev_base = 0;
   float prev_scale = 0.f, prev_cm = 0.f;
   int it = 0, stage = 0;
@@ -341,17 +374,8 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
         float a[8];
         const float4* hb = reinterpret_cast<const float4*>(Pb + (it & 1) * D);
         const float4 h0 = hb[0], h1 = hb[1];
-        a[0] = h0.x; a[1] = h0.y; a[2] = h0.z; a[3] = h0.w;
-        a[4] = h1.x; a[5] = h1.y; a[6] = h1.z; a[7] = h1.w;
-#pragma unroll
-        for (int c = 0; c < kTcMaxNib; ++c) {
-          if (c < p.nnib_row) {
-            const int r = (c * 16 + int((base >> p.nib_shift[c]) & 15u)) * 2;
-            const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);
-            a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
-            a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
-          }
-        }
+        a[0] = h0.x + ra[0]; a[1] = h0.y + ra[1]; a[2] = h0.z + ra[2]; a[3] = h0.w + ra[3];
+        a[4] = h1.x + ra[4]; a[5] = h1.y + ra[5]; a[6] = h1.z + ra[6]; a[7] = h1.w + ra[7];
         float2 P[D];
         sincos_red(a[K], &P[0].y, &P[0].x);
 #pragma unroll
@@ -385,9 +409,10 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
       epilogue(prev_base, prev_scale, prev_cm);
     }
 #if DSV_TC8_FILL == 0
-    // accumulators back to M for this tile's MMAs
+    // accumulators back to M for this tile's MMAs (8 columns per store from
+    // registers that stay live across the loop: no per-tile materialisation)
 #pragma unroll
-    for (int q = 0; q < 3 * N0 / 32; ++q) tmem_fill32(tlane + uint32_t(L::T_HI + 32 * q), kAccInit);
+    for (int q = 0; q < 3 * N0 / 8; ++q) tmem_st8(tlane + uint32_t(L::T_HI + 8 * q), mg);
 #endif
     // digits -> TMEM: column c holds K = 4c..4c+3 = (re, im) of members 2c, 2c+1
     uint32_t la2[N0 / 4], la1[N0 / 4], la0[N0 / 4];
@@ -432,6 +457,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
       mma_commit(bar);
     }
     coop_phase(it + 2, tq[S - 2 >= 1 ? 1 : 0]);
+    if (PHASED && !p.coop) row_angles(tq[0] | rowoff);  // tile i+1
     prev_base = base;
     prev_scale = scale;
     prev_cm = cm;
