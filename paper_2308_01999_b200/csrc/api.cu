@@ -59,6 +59,12 @@ const bool g_low_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// Warp-transposed phased k = 3 low-window kernel (low.cu k_dense_lowt); DSV_LOWT=0 disables.
+const bool g_lowt_env = [] {
+  const char* e = std::getenv("DSV_LOWT");
+  return !(e && e[0] == '0');
+}();
+
 // Warp-transpose kernel for dense gates inside the lowest 6 bits (wt.cu); DSV_WT=0 disables.
 const bool g_wt_env = [] {
   const char* e = std::getenv("DSV_WT");
@@ -575,7 +581,10 @@ int apply_low(dsv_state* s, const GateGeom& gg, const void* matrix, const std::v
   std::vector<cplx<float>> m;
   canon_matrix<float>(gg, matrix, m);
   ProfTok t = prof_start(s);
-  CKL(launch_dense_low(k, d, m.data(), s->gdata, s->d, s->stream), 1);
+  if (g_lowt_env && k == 3 && d.plain && s->nbits >= 12)
+    CKL(launch_dense_lowt(d, uint64_t(1) << s->nbits, m.data(), s->gdata, s->d, s->stream), 1);
+  else
+    CKL(launch_dense_low(k, d, m.data(), s->gdata, s->d, s->stream), 1);
   prof_stop(s, t, prof_class, bytes);
   return DSV_OK;
 }

@@ -151,6 +151,147 @@ k_dense_low(const __grid_constant__ LowP<K> p, const float4* __restrict__ tab, f
   }
 }
 
+// k = 3 without controls: each warp moves a contiguous 512-amplitude run
+// (4 KB, 16-byte coalesced loads) into its own shared-memory slice (16-byte
+// units XOR-swizzled by their 128-byte line: the group reads below are
+// conflict-free), every lane then applies the phase and the full 8 x 8 matrix
+// (kernel-parameter constant bank, warp-uniform FFMA operands) to two whole
+// groups, and the run streams back out.  No shuffles: ~45 instructions per
+// amplitude instead of ~80 for the lane-split kernel above.
+constexpr int kLowtRun = 512;  // amplitudes per warp run
+
+__device__ __forceinline__ uint32_t lowt_slot(uint32_t u) { return u ^ ((u >> 3) & 7u); }
+
+template <bool PHASED>
+__global__ void __launch_bounds__(256)
+k_dense_lowt(const __grid_constant__ LowP<3> p, uint64_t nruns, const float4* __restrict__ tab,
+             float4* __restrict__ sv4) {
+  extern __shared__ float4 lsm[];  // [8 warps][256 units] run slices, then [8][256] phase slots
+  float4* stab = lsm + 8 * 256;
+  if constexpr (PHASED) {
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) stab[i] = tab[i];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  float4* slice = lsm + warp * 256;
+  const uint64_t nwarps = uint64_t(gridDim.x) * 8;
+  for (uint64_t run = uint64_t(blockIdx.x) * 8 + warp; run < nruns; run += nwarps) {
+    float4* g4 = sv4 + run * (kLowtRun / 2);
+    float4 t[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[i] = __ldcs(g4 + i * 32 + lane);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) slice[lowt_slot(i * 32 + lane)] = t[i];
+    __syncwarp();
+    // index bytes 2..7 of the run: uniform
+    float4 hi = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint64_t rb = run * kLowtRun;
+    if constexpr (PHASED) {
+#pragma unroll
+      for (int c = 2; c < 8; ++c)
+        if ((p.used >> c) & 1u) {
+          const float4 x = stab[c * 256 + int((rb >> (8 * c)) & 255u)];
+          hi.x += x.x; hi.y += x.y; hi.z += x.z; hi.w += x.w;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int g = lane + 32 * q;  // group: amplitudes 8g .. 8g+7 of the run
+      float in[8][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 x = slice[lowt_slot(4 * g + c)];
+        in[2 * c][0] = x.x; in[2 * c][1] = x.y; in[2 * c + 1][0] = x.z; in[2 * c + 1][1] = x.w;
+      }
+      if constexpr (PHASED) {
+        float a[4] = {hi.x, hi.y, hi.z, hi.w};
+        const uint64_t b = rb + 8 * g;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          if ((p.used >> c) & 1u) {
+            const float4 x = stab[c * 256 + int((b >> (8 * c)) & 255u)];
+            a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+          }
+        float ang[8];
+        ang[0] = a[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+#pragma unroll
+          for (int j = 0; j < (1 << m); ++j) ang[j + (1 << m)] = ang[j] + a[m];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float sn, cs;
+          sincos_low(ang[j], &sn, &cs);
+          const float xr = in[j][0], xi = in[j][1];
+          in[j][0] = xr * cs - xi * sn;
+          in[j][1] = xr * sn + xi * cs;
+        }
+      }
+      float o[8][2];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        float re = 0.f, im = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float mr = p.m[r * 8 + c].x, mi = p.m[r * 8 + c].y;
+          re = fmaf(mr, in[c][0], re);
+          re = fmaf(-mi, in[c][1], re);
+          im = fmaf(mr, in[c][1], im);
+          im = fmaf(mi, in[c][0], im);
+        }
+        o[r][0] = re;
+        o[r][1] = im;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        slice[lowt_slot(4 * g + c)] = make_float4(o[2 * c][0], o[2 * c][1], o[2 * c + 1][0], o[2 * c + 1][1]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) __stcs(g4 + i * 32 + lane, slice[lowt_slot(i * 32 + lane)]);
+    __syncwarp();
+  }
+}
+
+template <bool PHASED>
+static cudaError_t lowt_go(const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab, void* sv,
+                           cudaStream_t st) {
+  LowP<3> p;
+  std::memset(&p, 0, sizeof p);
+  p.g = d.g;
+  p.nchunk = d.nchunk;
+  p.plain = d.plain;
+  for (int c = 0; c < d.nchunk; ++c) p.used |= 1u << (d.chunk_shift[c] / 8);
+  std::memcpy(p.m, matrix, sizeof(p.m));
+  const uint64_t nruns = namps / kLowtRun;
+  const int smem = (8 * 256 + (PHASED ? 8 * 256 : 0)) * 16;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_lowt<PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_lowt<PHASED>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t blocks = (nruns + 7) / 8;
+  const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_lowt<PHASED><<<unsigned(blocks), 256, smem, st>>>(p, nruns, static_cast<const float4*>(d_tab),
+                                                          static_cast<float4*>(sv));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_lowt(const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab, void* sv,
+                              cudaStream_t st) {
+  if (!d.plain || namps % kLowtRun) return cudaErrorInvalidValue;
+  return d.nchunk > 0 ? lowt_go<true>(d, namps, matrix, d_tab, sv, st) : lowt_go<false>(d, namps, matrix, d_tab, sv, st);
+}
+
 template <int K, bool PHASED>
 static cudaError_t low_go(const LowDesc& d, const void* matrix, const void* d_tab, void* sv, cudaStream_t st) {
   LowP<K> p;
