@@ -129,6 +129,35 @@ def test_tc_phased_vs_oracle(k):
         assert _rel_err(got, want) <= 2 * REL, (trial, _rel_err(got, want))
 
 
+@pytest.mark.parametrize("nrow", [0, 1, 2, 3, 4])
+def test_tc_phased_row_vectors_vs_oracle(nrow):
+    """Phase terms on 0..4 of a tile's row bits (the 7 lowest free bits) plus
+    tile-uniform bits: <= 3 row bits take the per-tile phase-vector path of
+    tc8.cu, 4 the per-row path — both against the oracle."""
+    rng = np.random.default_rng(1200 + nrow)
+    k = 5
+    for trial in range(3):
+        n = int(rng.integers(14, 19))
+        t0 = int(rng.integers(3, n - k - 2)) if trial != 2 else 1
+        targets = list(range(t0, t0 + k))
+        free = [q for q in range(n) if q not in targets]
+        rowbits, uniform = free[:7], free[7:]
+        pick = [int(b) for b in rng.choice(rowbits, size=nrow, replace=False)] if nrow else []
+        bits = pick + [int(b) for b in rng.choice(uniform, size=min(4, len(uniform)), replace=False)]
+        cross = [(int(rng.integers(0, k)), b, float(rng.uniform(-7, 7))) for b in bits for _ in range(2)]
+        outside = [(b, float(rng.uniform(-7, 7))) for b in bits]
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng).astype(np.complex64)
+        want = st.astype(np.complex128) * np.exp(1j * _phase_angles(n, targets, cross, outside))
+        O.apply_dense(want, n, m.astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.native.apply_matrix_phased(m, targets, cross, outside)
+        sv._mutated()
+        assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1
+        assert _rel_err(sv.amplitudes, want) <= 2 * REL, (trial, _rel_err(sv.amplitudes, want))
+
+
 def test_tc_involution_round_trip_large():
     """U then U^dagger on a 24-qubit state with a target in every position
     class (low/mid/high): returns the input to fp32-level accuracy."""
