@@ -1248,6 +1248,18 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
     prof_stop(s, t, PC_PERM, bytes);
     return DSV_OK;
   }
+  if (g_wt_env && nctrl == 0 && k >= 1 && k <= (s->dtype == DSV_C128 ? 3 : 4) && gg.tsorted[k - 1] < 6 &&
+      gg.tsorted[0] <= 1 && s->nbits >= 10) {
+    // targets on index bits 0/1 and all below 6: the register path's lanes sit
+    // >= 32 bytes apart (perm2 on (0,1) measured 0.59): warp-transposed runs
+    uint64_t active = 0;
+    for (uint64_t j = 0; j < D; ++j)
+      if (act[j]) active |= 1ull << j;
+    ProfTok t = prof_start(s);
+    CKL(launch_perm_wt(s->dtype, s->nbits, k, gg.tsorted.data(), pn.data(), dn.data(), active, s->d, s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
   if (k <= kPermRegMaxK) {
     UnitView uv;
     if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;

@@ -72,6 +72,9 @@ cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const 
                              cudaStream_t st);
 // k <= 3 (complex128) / 4 (complex64) dense gate, all targets < 6, no controls:
 // per-warp shared-memory transpose of contiguous runs (tb = sorted target bits)
+// generalised permutation with all targets in bits 0..5 (no controls), warp-transposed (wt.cu)
+cudaError_t launch_perm_wt(int dtype, int nbits, int k, const int* tb, const uint64_t* pout, const void* diag,
+                           uint64_t active, void* sv, cudaStream_t st);
 cudaError_t launch_dense_wt(int dtype, int nbits, int k, const int* tb, const void* matrix, void* sv,
                             cudaStream_t st);
 // k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem

@@ -282,6 +282,30 @@ def test_genperm_and_diag_all_arities_bit_exact(dtype, k):
 
 
 @pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_genperm_low_bits_warp_transposed_bit_exact(dtype, k):
+    """Permutation tables whose targets lie in bits 0..5 and touch bit 0 or 1
+    (the warp-transposed kernel, wt.cu k_perm_wt): bit-exact vs the oracle."""
+    if dtype == np.complex128 and k == 4:
+        pytest.skip("complex128 runs hold 256 amplitudes: k <= 3")
+    rng = np.random.default_rng(300 + k)
+    for trial in range(5):
+        n = int(rng.integers(10, 15))
+        targets = [int(rng.integers(0, 2))] + [int(x) for x in rng.choice(
+            [b for b in range(6) if b > 1], size=k - 1, replace=False)]
+        targets = [int(x) for x in rng.permutation(targets)]
+        st = random_state(n, rng, dtype)
+        diag = np.exp(1j * rng.uniform(0, 2 * np.pi, 1 << k))
+        diag[rng.random(1 << k) < 0.3] = 1.0
+        perm = rng.permutation(1 << k)
+        want = st.copy()
+        O.apply_genperm(want, n, perm, diag, targets, [])
+        sv = sv_from(st)
+        sv.apply_generalized_permutation(G.PermutationGate(perm, diag, tuple(targets)))
+        _check(sv.amplitudes, want, dtype, exact=True)
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
 def test_swaps_many_pairs_bit_exact(dtype):
     rng = np.random.default_rng(5)
     for n in (2, 3, 7, 12, 16):
