@@ -91,10 +91,17 @@ class _Phase:
 
 def _phase_poly(g: Gate) -> _Phase | None:
     """Phase-polynomial form of a <= 2-qubit unit-modulus diagonal, else None."""
-    if not isinstance(g, PermutationGate) or not g.is_diagonal:
+    if not isinstance(g, PermutationGate):
         return None
     qs = list(g.targets) + [q for q, _ in g.controls]
-    if len(qs) > 2 or np.max(np.abs(np.abs(g.diagonal) - 1.0)) > 1e-12:
+    if len(qs) > 2:
+        return None
+    # tiny tables: Python scalars beat NumPy's per-call overhead (577 gates per QFT-33)
+    perm = g.permutation.tolist()
+    if perm != list(range(len(perm))):
+        return None
+    diag = g.diagonal.tolist()
+    if any(abs(abs(z) - 1.0) > 1e-12 for z in diag):
         return None
     pos = {q: i for i, q in enumerate(qs)}
 
@@ -105,7 +112,7 @@ def _phase_poly(g: Gate) -> _Phase | None:
         j = 0
         for m, q in enumerate(g.targets):
             j |= ((x >> pos[q]) & 1) << m
-        return complex(g.diagonal[j])
+        return diag[j]
 
     if len(qs) == 1:
         c = cmath.phase(entry(0))
@@ -116,7 +123,7 @@ def _phase_poly(g: Gate) -> _Phase | None:
 
 def _is_swap(g: Gate) -> bool:
     return (isinstance(g, PermutationGate) and not g.controls and len(g.targets) == 2
-            and list(g.permutation) == [0, 2, 1, 3] and np.all(g.diagonal == 1))
+            and g.permutation.tolist() == [0, 2, 1, 3] and g.diagonal.tolist() == [1, 1, 1, 1])
 
 
 def _diag_gate(qubits, const: float, lin: dict, quad: float) -> PermutationGate:
@@ -161,12 +168,16 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
         pending: list[tuple[int, bool]] = []  # left-behind phases (index, movable)
         taken: set[int] = set()
 
+        fixed_q: set[int] = set()         # qubits of non-movable pending phases
+
         def absorb_pending(qs):
             """Movable pending phases touching qubits that join W become
             pre-phases (they precede every member acting on those qubits)."""
+            if not any(mov for _, mov in pending):
+                return
             keep = []
             for pi, mov in pending:
-                if mov and qset(pi) & qs:
+                if mov and not qsets[pi].isdisjoint(qs):
                     pre.append(pi)
                     taken.add(pi)
                 else:
@@ -174,7 +185,7 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
             pending[:] = keep
 
         def blocked_by_pending(qs) -> bool:
-            return any((not mov) and (qset(pi) & qs) for pi, mov in pending)
+            return not fixed_q.isdisjoint(qs)
 
         for i in remaining:
             qs = qset(i)
@@ -187,6 +198,7 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
                     continue
                 if qs & left_nd:
                     pending.append((i, False))
+                    fixed_q |= qs
                 elif not (qs & acted):
                     if qs & W:
                         pre.append(i)          # precedes every member on its qubits
@@ -205,6 +217,7 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
                         taken.add(i)
                     else:
                         pending.append((i, False))
+                        fixed_q |= qs
                 continue
             # matrix gate
             if i == g0:
@@ -296,10 +309,17 @@ def _emit_window(gates, phases, members: list[int], pre: list[int], W: set[int])
                 cross[(ta, ob)] = cross.get((ta, ob), 0.0) + ph.quad
     prod = np.diag(inner_pre * cmath.exp(1j * const))
     for i in members:
-        g = gates[i]
-        if phases[i] is not None:
-            g = _diag_gate(phases[i].qubits, phases[i].const, phases[i].lin, phases[i].quad)
-        prod = expand_gate(g, union) @ prod
+        ph = phases[i]
+        if ph is not None:  # internal phase: scale the rows (no 2^m x 2^m product)
+            ang = np.full(cols.size, ph.const)
+            for q, t in ph.lin.items():
+                ang += t * ((cols >> pos[q]) & 1)
+            if len(ph.qubits) == 2 and ph.quad != 0.0:
+                a, b = ph.qubits
+                ang += ph.quad * (((cols >> pos[a]) & 1) & ((cols >> pos[b]) & 1))
+            prod *= np.exp(1j * ang)[:, None]
+            continue
+        prod = expand_gate(gates[i], union) @ prod
     if not cross and not outside:
         return DenseGate(prod, tuple(union), unitary=False)
     return PhasedDenseGate(prod, tuple(union), [(a, b, t) for (a, b), t in cross.items()],
