@@ -442,7 +442,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
   int e_b = 0;
   if (bmax > 0.f) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
-  if (g_tc8_env && k <= 5 && e_b >= -20 && e_b <= 20) {
+  if (g_tc8_env && k <= 6 && e_b >= -20 && e_b <= 20) {
     // 8-bit digits (tc8.cu): X = B 2^(23 - e_b) rounded, X + 0x8080 split into
     // balanced base-256 digits b2 (2^16), b1 (2^8), b0 in [-128, 127];
     // rows [b2 | b1 | b0] x (n = 2i + out re/im), 128 bytes of K = 2j + in re/im
@@ -484,7 +484,10 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
     d.htab = reinterpret_cast<const float*>(host.data() + bbytes);
     ProfTok t = prof_start(s);
-    CKL(launch_dense_tc8(k, d, d_b, d_b + bbytes, s->d, s->stream), 1);
+    if (k == 6)
+      CKL(launch_dense_tc68(d, d_b, d_b + bbytes, s->d, s->stream), 1);
+    else
+      CKL(launch_dense_tc8(k, d, d_b, d_b + bbytes, s->d, s->stream), 1);
     prof_stop(s, t, prof_class, bytes);
     return DSV_OK;
   }

@@ -48,6 +48,8 @@ struct TcDesc {
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);
 int tc_smem_bytes(int k);
+// k = 6 windows through 8-bit integer digits (tc68.cu); d_bmat = [b2 | b1 | b0][128 rows][128] int8
+cudaError_t launch_dense_tc68(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st);
 // same windows through 8-bit integer digits (tc8.cu); d_bmat = [b2 | b1 | b0][2^(k+1) rows][128] int8
 cudaError_t launch_dense_tc8(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                              cudaStream_t st);
