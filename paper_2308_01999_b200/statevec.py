@@ -322,21 +322,27 @@ class StateVector:
     # a 33-qubit state never needs a host copy of the whole vector
     DUMP_CHUNK = 1 << 24
 
+    def logical_chunks(self, chunk: int | None = None):
+        """Yield the logical-order amplitudes in consecutive chunks (gathered
+        on the GPU), so callers can stream a state larger than host memory."""
+        n = self.num_qubits
+        chunk = chunk or self.DUMP_CHUNK
+        identity = self.bit_map == list(range(n))
+        self._sync_in()
+        for begin in range(0, 1 << n, chunk):
+            end = min(1 << n, begin + chunk)
+            if identity:
+                yield self._dev.download(begin=begin, count=end - begin)
+            else:
+                yield self._dev.access_get(list(self.bit_map), begin, end)
+
     def dump(self, path) -> None:
         """``<Q`` qubit count, then interleaved little-endian float64 (re, im)
         in logical order — always float64, also for complex64 states
         (statevec.py:332-340 format)."""
-        n = self.num_qubits
-        identity = self.bit_map == list(range(n))
-        self._sync_in()
         with open(path, "wb") as fh:
-            fh.write(struct.pack("<Q", n))
-            for begin in range(0, 1 << n, self.DUMP_CHUNK):
-                end = min(1 << n, begin + self.DUMP_CHUNK)
-                if identity:
-                    chunk = self._dev.download(begin=begin, count=end - begin)
-                else:
-                    chunk = self._dev.access_get(list(self.bit_map), begin, end)
+            fh.write(struct.pack("<Q", self.num_qubits))
+            for chunk in self.logical_chunks():
                 fh.write(chunk.astype(np.complex128).view("<f8").tobytes())
 
     @classmethod

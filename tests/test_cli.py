@@ -78,3 +78,16 @@ class TestSimulateGPU:
         _, rep1 = run_json(capsys, *args)
         _, rep2 = run_json(capsys, *args)
         assert masked(rep1) == masked(rep2)
+
+    def test_streamed_digest_matches_full(self, capsys, monkeypatch):
+        """Large states stream the digest and norm chunk by chunk: same values."""
+        from paper_2308_01999_b200 import cli
+        from paper_2308_01999_b200.statevec import StateVector
+
+        args = ("simulate", "--circuit", "qv", "--n", "12", "--engine", "sv", "--seed", "3", "--dtype", "c64")
+        _, full = run_json(capsys, *args)
+        monkeypatch.setattr(cli, "STREAM_QUBITS", 4)
+        monkeypatch.setattr(StateVector, "DUMP_CHUNK", 1 << 7)
+        _, streamed = run_json(capsys, *args)
+        assert streamed["digest"] == full["digest"]
+        assert abs(streamed["counters"]["norm"] - full["counters"]["norm"]) < 1e-9
