@@ -125,9 +125,12 @@ def cmd_simulate(args) -> int:
         return EXIT_OK
 
     ops = fused_ops(args, to_gates(circuit), counters, timings)
-    t0 = time.perf_counter()
     if args.engine == "sv":
+        t0 = time.perf_counter()
         sv = StateVector(n, dtype=dtype, device=args.device)
+        sv.native.sync()
+        timings["alloc_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
         nat = sv.native
         nat.prof_enable(True)
         for g in ops:
@@ -155,6 +158,7 @@ def cmd_simulate(args) -> int:
             return EXIT_OK
         amps = sv.logical_amplitudes()
     else:
+        t0 = time.perf_counter()
         with SegmentedStateVector(n, args.global_bits, args.workers, dtype=dtype) as ssv:
             segs = ssv.native_segments
             for s in segs:
