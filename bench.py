@@ -309,7 +309,14 @@ def run_single(args) -> None:
     d2h = 0
     for i in range(max(1, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
-        f2 = fuse_ops(gates, args.fusion)
+        if args.fusion == "fold":
+            # windows stream out of the fuser as it closes them: the GPU runs
+            # window i while the host fuses window i + 1
+            from paper_2308_01999_b200.fusion_fold import fold_ops
+
+            f2 = fold_ops(gates, FOLD_K)
+        else:
+            f2 = fuse_ops(gates, args.fusion)
         sv = run_circuit_sv(f2, N_QUBITS, dtype=np.complex64, device=dev)
         p = sv.probabilities([0, 1, 2, 3])
         d2h = p.nbytes
@@ -352,7 +359,7 @@ def run_single(args) -> None:
         "cpu_baseline": cpu,
         "e2e": {"value": len(gates) / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
-                "path": "fuse + StateVector alloc + run_circuit_sv + probabilities([0..3])"},
+                "path": "fuse (streamed: fold_ops feeds run_circuit_sv) + StateVector alloc + run_circuit_sv + probabilities([0..3])"},
         "gpu_launches": launches,
         "clocks": clk,
         "kernels": kernels,

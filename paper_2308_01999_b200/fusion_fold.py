@@ -140,6 +140,26 @@ def _diag_gate(qubits, const: float, lin: dict, quad: float) -> PermutationGate:
 
 def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: int = 10,
               relabel_swaps: bool = True) -> FoldedCircuit:
+    ops: list = []
+    prov: list[list[int]] = []
+    for op, pv in fuse_fold_iter(circuit, max_gate_size, max_diag_size, relabel_swaps):
+        ops.append(op)
+        prov.append(pv)
+    return FoldedCircuit(ops, prov)
+
+
+def fold_ops(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: int = 10,
+             relabel_swaps: bool = True):
+    """The fused ops one at a time, as the fuser closes each window: feeding
+    them straight to ``run_circuit_sv`` overlaps host fusion with the GPU
+    running the windows already emitted."""
+    for op, _ in fuse_fold_iter(circuit, max_gate_size, max_diag_size, relabel_swaps):
+        yield op
+
+
+def fuse_fold_iter(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: int = 10,
+                   relabel_swaps: bool = True):
+    """Generator form of :func:`fuse_fold`: yields (op, provenance) pairs."""
     k = int(max_gate_size)
     if not 1 <= k <= 10 or not 1 <= max_diag_size <= 12:
         raise InvalidArgumentError("fusion sizes out of range")
@@ -147,8 +167,6 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
     phases = [_phase_poly(g) for g in gates]
     swaps = [relabel_swaps and _is_swap(g) for g in gates]
     remaining = list(range(len(gates)))
-    ops: list = []
-    prov: list[list[int]] = []
 
     qsets = [frozenset(g.qubits) for g in gates]  # computed once: the scan below revisits gates
 
@@ -241,11 +259,9 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
         remaining = [i for i in remaining if i not in taken]
         if standalone:
             if pre:
-                ops.append(_diag_window([gates[i] for i in pre], None))
-                prov.append(sorted(pre))
+                yield _diag_window([gates[i] for i in pre], None), sorted(pre)
             g = gates[g0]
-            ops.append(QubitSwap(*g.targets) if swaps[g0] else g)
-            prov.append([g0])
+            yield (QubitSwap(*g.targets) if swaps[g0] else g), [g0]
             continue
         # movable single-qubit phases on outside qubits ride along as outside terms
         for pi, mov in pending:
@@ -253,14 +269,11 @@ def fuse_fold(circuit: Sequence[Gate], max_gate_size: int = 5, max_diag_size: in
                 pre.append(pi)
                 taken.add(pi)
         remaining = [i for i in remaining if i not in taken]
-        ops.append(_emit_window(gates, phases, members, pre, W))
-        prov.append(sorted(members + pre))
+        yield _emit_window(gates, phases, members, pre, W), sorted(members + pre)
     # leftover phase gates: commute with everything after them -> diagonal windows
     if remaining:
         for chunk in _pack_diagonals(remaining, gates, max_diag_size):
-            ops.append(_fused_diagonal([gates[i] for i in chunk], sorted({q for i in chunk for q in gates[i].qubits})))
-            prov.append(chunk)
-    return FoldedCircuit(ops, prov)
+            yield _fused_diagonal([gates[i] for i in chunk], sorted({q for i in chunk for q in gates[i].qubits})), chunk
 
 
 def _diag_window(gs, phs):
