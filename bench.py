@@ -4,17 +4,19 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Workload (BASELINE.json configs[2], the config its metric is quoted on):
-33-qubit QFT (577 gates) in complex64 (64 GiB state), host gate fusion with
-FusionConfig(max_fused_gate_size=5, max_fused_diagonal_gate_size=6) -> 152
-fused ops, run from |0...0> on one B200.  A "step" = reset to |0> + the whole
-fused circuit.  At N > 1 (torchrun, one process per GPU) the same 33-qubit
+33-qubit QFT (577 gates) in complex64 (64 GiB state), host gate fusion up to
+k = 5 with the phase-folding fuser (fusion_fold.py: 7 dense/phased windows,
+SWAPs as relabels; the reference's FusionConfig(5, 6) gives 152 ops and is
+timed beside it), run from |0...0> on one B200.  A "step" = reset to |0> +
+the whole fused circuit.  At N > 1 (torchrun, one process per GPU) the same 33-qubit
 circuit is sharded over N GPUs by its top log2 N qubits (strong scaling, as
 in the paper's PAPER.md:285-298 table) with P2P global<->local swaps.
 
 value   = circuit gates (577) / device time per step (CUDA events on the
           state's stream, max over ranks), inputs resident in HBM;
-e2e     = the same metric through the public Python API (fuse + StateVector
-          alloc + run_circuit + probabilities read-back), host wall clock;
+e2e     = the same metric through the public Python API (fuse, streamed into
+          run_circuit_sv + StateVector alloc + probabilities read-back),
+          host wall clock;
 roofline= dominant kernel class: algorithmic bytes / its CUDA-event time vs
           the measured HBM copy peak (MEASURED_PEAKS.json);
 cpu_baseline = the CPU oracle port of the reference algorithm on this host.

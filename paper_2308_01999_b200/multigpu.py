@@ -365,6 +365,23 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
     ms_step = ms_total / args.steps
     value = len(gates) / (ms_step / 1000.0)
     p = dsv.probabilities([0, 1, 2, 3])
+    # e2e through the public API, host wall clock, max over ranks: fuse on the
+    # host (every rank), reset to |0>, run with P2P swaps, probabilities read-back
+    from .fusion_fold import fuse_fold
+
+    e2e = []
+    for i in range(3):
+        comm.barrier()
+        t0 = time.perf_counter()
+        ops2 = fuse_fold(gates, 5).ops if getattr(args, "fusion", "fold") == "fold" else ops
+        dsv.reset()
+        dsv.run(ops2)
+        p = dsv.probabilities([0, 1, 2, 3])
+        dt = comm.allreduce_max(time.perf_counter() - t0)
+        if i > 0:
+            e2e.append(dt)
+    e2e_s = sorted(e2e)[len(e2e) // 2]
+    gate_bytes = sum(int(getattr(g, "matrix", np.zeros(0)).size) * 8 for g in ops)
     if comm.rank == 0:
         pk = peaks()
         dom_name, dom_v = max(prof.items(), key=lambda kv: kv[1]["ms"])
@@ -381,8 +398,10 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None},
             "transfer_stats": dsv.stats.as_dict(),
-            "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": p.nbytes,
-                    "note": "multi-GPU e2e = device-resident run + probabilities read-back"},
+            "e2e": {"value": len(gates) / e2e_s, "unit": "gates/s", "seconds_per_step": e2e_s,
+                    "h2d_bytes_per_step": gate_bytes, "d2h_bytes_per_step": p.nbytes,
+                    "path": "fuse_fold + DistributedStateVector.reset/run + probabilities([0..3]), "
+                            "wall clock, max over ranks"},
             "gpu_launches": launches_all,
             "clocks": clk,
             "check_prob_sum": float(p.sum()),
