@@ -189,6 +189,28 @@ class DistributedStateVector:
         """|0...0> with the identity qubit map."""
         self.seg.set_basis(0 if self.rank == 0 else None)
         self.qubit_map = list(range(self.num_qubits))
+        self._basis0 = True
+
+    def _place_for(self, gates) -> None:
+        """|0...0> is invariant under any relabelling of index bits, so before
+        the first gate the qubit map is free: put on the global bits the
+        qubits whose first use as a target comes last (never: first).  A QFT
+        then needs one global<->local reorder instead of two (no data moves
+        here: only the map changes)."""
+        n, nloc = self.num_qubits, self.local_bits
+        first: dict[int, int] = {}
+        for i, g in enumerate(gates):
+            for q in getattr(g, "targets", ()):
+                first.setdefault(q, i)
+        order = sorted(range(n), key=lambda q: (-first.get(q, len(gates) + 1), -q))
+        glob = order[: n - nloc]
+        loc = [q for q in range(n) if q not in glob]
+        qmap = [0] * n
+        for b, q in enumerate(loc):
+            qmap[q] = b
+        for j, q in enumerate(sorted(glob)):
+            qmap[q] = nloc + j
+        self.qubit_map = qmap
 
     def distributed_index_bit_swap(self, pairs: Sequence[tuple[int, int]]) -> None:
         check_swap_pairs(pairs)
@@ -222,6 +244,7 @@ class DistributedStateVector:
     def apply(self, g: Gate, upcoming=()) -> None:
         from .fusion_fold import PhasedDenseGate, QubitSwap
 
+        self._basis0 = False
         if isinstance(g, QubitSwap):  # relabel only: no data moves on any rank
             self.qubit_map[g.a], self.qubit_map[g.b] = self.qubit_map[g.b], self.qubit_map[g.a]
             return
@@ -245,6 +268,8 @@ class DistributedStateVector:
 
     def run(self, gates) -> None:
         gates = list(gates)
+        if getattr(self, "_basis0", False) and self.global_bits > 0:
+            self._place_for(gates)
         for i, g in enumerate(gates):
             self.apply(g, gates[i + 1:])
 
