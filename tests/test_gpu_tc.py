@@ -76,6 +76,27 @@ def test_tc_dense_vs_oracle(k):
         assert _rel_err(got, want) <= REL, (trial, targets, ctrls, _rel_err(got, want))
 
 
+@pytest.mark.parametrize("k", [4, 5, 6])
+@pytest.mark.parametrize("scale", [2.0 ** -12, 0.37, 3.1, 2.0 ** 9])
+def test_tc_scaled_matrices_and_tiny_states(k, scale):
+    """Non-unitary (scaled) gate matrices move the gate exponent e_b; a state
+    scaled by 2^-60 moves every row exponent: the digit scaling must follow
+    both (relative error unchanged)."""
+    rng = np.random.default_rng(int(1000 * scale) + k)
+    n = 16
+    targets = list(range(4, 4 + k)) if k != 4 else [0, 1, 2, 3]
+    m = (G.random_unitary(1 << k, rng) * scale).astype(np.complex64)
+    for amp_scale in (1.0, 2.0 ** -60):
+        st = (random_state(n, rng, np.complex64) * np.float32(amp_scale)).astype(np.complex64)
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(np.complex128), targets, [])
+        sv = StateVector.from_amplitudes(st)
+        nat = _tc_launches(sv)
+        sv.apply_matrix(G.DenseGate(m, tuple(targets), unitary=False))
+        assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1
+        assert _rel_err(sv.amplitudes, want) <= 2 * REL, (amp_scale, _rel_err(sv.amplitudes, want))
+
+
 @pytest.mark.parametrize("case", ["low0", "low0c", "bit1", "ctrl0", "spread0"])
 def test_tc_dense_low_bits_vs_oracle(case):
     """Index bit 0 a target or control: the 8-byte-per-row (non-pair) copies."""
