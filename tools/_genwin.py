@@ -1,0 +1,17 @@
+import sys, statistics
+sys.path.insert(0, '.')
+import numpy as np
+from paper_2308_01999_b200.statevec import StateVector
+from paper_2308_01999_b200 import gates as G
+from tools.sweep import peak
+n = 33; pk = peak(); rng = np.random.default_rng(0)
+sv = StateVector(n, dtype=np.complex64); nat = sv.native
+for q in range(n): sv.apply(G.DenseGate(G.random_unitary(2, rng), (q,)))
+m = G.random_unitary(32, rng)
+for tg in [(8, 9, 10, 11, 12), (3, 9, 15, 21, 27), (2, 7, 13, 20, 30), (1, 5, 9, 13, 17), (0, 5, 10, 15, 20), (28, 29, 30, 31, 32)]:
+    op = G.DenseGate(m, tg)
+    ts = []
+    for _ in range(5):
+        nat.event_record(0); sv.apply(op); nat.event_record(1); ts.append(nat.event_elapsed(0, 1))
+    ms = statistics.median(ts[1:])
+    print(tg, f"{ms:.2f} ms {16*(1<<n)/ms/1e6/pk:.2f}", flush=True)
