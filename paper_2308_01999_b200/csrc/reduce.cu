@@ -301,6 +301,75 @@ k_expect_pauli(const V* __restrict__ sv, uint64_t npairs, const __grid_constant_
   }
 }
 
+// complex64 strings with an X/Y: pairs (i, i ^ x) read as 16-byte units (two
+// adjacent amplitudes each), half the load instructions of the pair kernel
+// above.  Unit u holds amplitudes 2u, 2u + 1; with x' = x >> 1 the partner
+// unit is u ^ x', and when x flips bit 0 the partners swap halves (x' = 0:
+// the pair lies inside one unit).
+template <bool FLIP0, bool SELF>
+__global__ void __launch_bounds__(kReduceThreads)
+k_expect_pauli4(const float4* __restrict__ sv, uint64_t nwork, const __grid_constant__ PauliOp op,
+                double* __restrict__ partial) {
+  __shared__ double sh[kReduceThreads / 32];
+  const uint64_t xu = op.xmask >> 1;
+  const int hu = SELF ? 0 : 63 - __clzll(xu);
+  const uint64_t lowmask = SELF ? 0 : (1ull << hu) - 1ull;
+  double er = 0.0, ei = 0.0;
+  const uint64_t t0 = uint64_t(blockIdx.x) * kChunkUnits + threadIdx.x;
+  constexpr int kBatch = 8;
+  const float obr = float(op.br), obi = float(op.bi);
+#pragma unroll 1
+  for (int u0 = 0; u0 < kReduceUnitsPerThread; u0 += kBatch) {
+    float4 a[kBatch], b[kBatch];
+    uint64_t ii[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t t = t0 + uint64_t(u0 + u) * kReduceThreads;
+      const bool on = t < nwork;
+      const uint64_t i = SELF ? t : (((t & ~lowmask) << 1) | (t & lowmask));
+      ii[u] = i;
+      a[u] = on ? ldg_s(sv + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (!SELF) b[u] = on ? ldg_s(sv + (i ^ xu)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float br_ = 0.f, bi_ = 0.f;
+    auto pair = [&](float ar, float ai, uint64_t ia, float bre, float bim, uint64_t jb) {
+      const float si = (__popcll(ia & op.yzmask) & 1) ? -1.f : 1.f;
+      const float sj = (__popcll(jb & op.yzmask) & 1) ? -1.f : 1.f;
+      // q = B b ; term_i = conj(a) q si    q' = B a ; term_j = conj(b) q' sj
+      const float qr = obr * bre - obi * bim, qi = obr * bim + obi * bre;
+      br_ += si * (ar * qr + ai * qi);
+      bi_ += si * (ar * qi - ai * qr);
+      const float pr = obr * ar - obi * ai, pim = obr * ai + obi * ar;
+      br_ += sj * (bre * pr + bim * pim);
+      bi_ += sj * (bre * pim - bim * pr);
+    };
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint64_t i2 = ii[u] << 1;
+      if constexpr (SELF) {  // x = 1: amplitudes 2u, 2u + 1 of the same unit
+        pair(a[u].x, a[u].y, i2, a[u].z, a[u].w, i2 + 1);
+      } else {
+        const uint64_t j2 = (ii[u] ^ xu) << 1;
+        if constexpr (FLIP0) {
+          pair(a[u].x, a[u].y, i2, b[u].z, b[u].w, j2 + 1);
+          pair(a[u].z, a[u].w, i2 + 1, b[u].x, b[u].y, j2);
+        } else {
+          pair(a[u].x, a[u].y, i2, b[u].x, b[u].y, j2);
+          pair(a[u].z, a[u].w, i2 + 1, b[u].z, b[u].w, j2 + 1);
+        }
+      }
+    }
+    er += double(br_);
+    ei += double(bi_);
+  }
+  const double sr = block_sum<kReduceThreads>(er, sh);
+  const double si = block_sum<kReduceThreads>(ei, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = sr;
+    partial[2 * blockIdx.x + 1] = si;
+  }
+}
+
 // Z-only strings (no bit flip): sum of +-|a_i|^2 over 16-byte units (two
 // complex64 / one complex128 amplitude), per-batch sums in the state's
 // precision folded into fp64.
@@ -357,6 +426,20 @@ cudaError_t launch_expect_pauli(int dtype, int nbits, const PauliOp& op, const v
     else
       k_expect_z<float><<<unsigned(blocks), kReduceThreads, 0, st>>>(static_cast<const float4*>(sv), nunits,
                                                                      op.yzmask, d_partial);
+    return cudaGetLastError();
+  }
+  if (dtype == 0 && op.hbit >= 0 && n >= 8) {
+    const float4* s4 = static_cast<const float4*>(sv);
+    const bool flip0 = op.xmask & 1ull, self = (op.xmask >> 1) == 0;
+    const uint64_t nwork = self ? n / 2 : n / 4;  // units (x = 1) or unit pairs
+    const uint64_t blocks = chunks_for(nwork);
+    *nchunks_out = blocks;
+    if (self)
+      k_expect_pauli4<true, true><<<unsigned(blocks), kReduceThreads, 0, st>>>(s4, nwork, op, d_partial);
+    else if (flip0)
+      k_expect_pauli4<true, false><<<unsigned(blocks), kReduceThreads, 0, st>>>(s4, nwork, op, d_partial);
+    else
+      k_expect_pauli4<false, false><<<unsigned(blocks), kReduceThreads, 0, st>>>(s4, nwork, op, d_partial);
     return cudaGetLastError();
   }
   const uint64_t npairs = op.hbit >= 0 ? n / 2 : n;
