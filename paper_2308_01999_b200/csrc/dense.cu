@@ -191,27 +191,33 @@ k_expect_dense(const __grid_constant__ DenseP<K, typename VT::R> p,
     V in[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) in[j] = ldg_s(sv + base + p.offs[j]);
+    // the group's psi^dagger M psi in the state's precision (fp32 for
+    // complex64: the fp64 pipe and float->double converts stay off the
+    // per-element path), one fp64 add per group
+    R gr = R(0), gi = R(0);
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      double accr = 0.0, acci = 0.0;
+      R accr = R(0), acci = R(0);
 #pragma unroll
       for (int c = 0; c < D; ++c) {
         R ar, ai;
         VT::get(in[c], 0, ar, ai);
-        const double mr = double(p.m[r * D + c].x), mi = double(p.m[r * D + c].y);
-        accr = fma(mr, double(ar), accr);
-        accr = fma(-mi, double(ai), accr);
-        acci = fma(mr, double(ai), acci);
-        acci = fma(mi, double(ar), acci);
+        const R mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
+        accr = fma(mr, ar, accr);
+        accr = fma(-mi, ai, accr);
+        acci = fma(mr, ai, acci);
+        acci = fma(mi, ar, acci);
       }
       R xr, xi;
       VT::get(in[r], 0, xr, xi);
       // conj(x) * acc
-      er = fma(double(xr), accr, er);
-      er = fma(double(xi), acci, er);
-      ei = fma(double(xr), acci, ei);
-      ei = fma(-double(xi), accr, ei);
+      gr = fma(xr, accr, gr);
+      gr = fma(xi, acci, gr);
+      gi = fma(xr, acci, gi);
+      gi = fma(-xi, accr, gi);
     }
+    er += double(gr);
+    ei += double(gi);
   }
   const double sr = block_sum<256>(er, sh);
   const double si = block_sum<256>(ei, sh);
