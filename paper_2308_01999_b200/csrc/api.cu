@@ -1464,7 +1464,7 @@ int dsv_access_set(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64
 // ---- reductions -----------------------------------------------------------------------------
 
 static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2, double* host_out,
-                      double** d_partial_out, uint64_t* nchunks_out) {
+                      double** d_partial_out, uint64_t* nchunks_out, uint64_t* chunk_amps_out = nullptr) {
   if (k < 0 || k > 26) return fail(DSV_EUNSUPPORTED, "marginal over %d bits not supported (max 26)", k);
   uint64_t seen = 0;
   for (int j = 0; j < k; ++j) {
@@ -1482,9 +1482,9 @@ static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2,
     std::memset(&bg1, 0, sizeof bg1);
     bg1.reg_j = -1;
     std::vector<int> oholes;
-    // (sampling asks for the per-chunk partials in amplitude-contiguous
-    // chunks of its own size: it keeps the original kernel)
-    bool ok = s->nbits >= ib_bits && d_partial_out == nullptr;
+    // (chunk partials for sampling: only without binning, where chunk c is
+    // the amplitude-contiguous run of kReduceThreads * kReduceUnitsPerThread units)
+    bool ok = s->nbits >= ib_bits && (d_partial_out == nullptr || (k == 0 && chunk_amps_out));
     for (int j = 0; j < k && ok; ++j) {
       const int b = bits[j];
       if (b < ib_bits) {
@@ -1524,6 +1524,7 @@ static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2,
       if (d_partial_out) {
         *d_partial_out = d_partial;
         *nchunks_out = bg1.nchunks;
+        *chunk_amps_out = uint64_t(kReduceThreads) * kReduceUnitsPerThread * (s->dtype == DSV_C64 ? 2 : 1);
         return DSV_OK;
       }
       return finish_reduce(s, nbins, bg1.nchunks, 1, d_partial, d_out, host_out);
@@ -1700,8 +1701,8 @@ int dsv_sample(dsv_state* s, const double* variates, int64_t shots, uint64_t* ou
   // 1) ordered chunk sums of |a|^2 over kChunk-amplitude chunks (scalar units)
   double* d_partial = nullptr;
   uint64_t nch = 0;
-  if (int rc = probs_impl(s, nullptr, 0, false, nullptr, &d_partial, &nch)) return rc;
-  const uint64_t chunk_amps = uint64_t(kReduceThreads) * kReduceUnitsPerThread;
+  uint64_t chunk_amps = uint64_t(kReduceThreads) * kReduceUnitsPerThread;  // scalar-unit fallback
+  if (int rc = probs_impl(s, nullptr, 0, false, nullptr, &d_partial, &nch, &chunk_amps)) return rc;
   std::vector<double> cs(nch);
   CK(cudaMemcpyAsync(cs.data(), d_partial, sizeof(double) * nch, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
