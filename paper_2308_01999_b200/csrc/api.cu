@@ -1631,7 +1631,9 @@ int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, 
   DeviceGuard g(s->device);
   if (k <= 4) {
     UnitView uv;
-    if (int rc = unit_view(s, gg, false, &uv)) return rc;
+    // 16-byte units (two groups per thread) when bit 0 is free, up to k = 3
+    // (k = 4 with two groups per thread exceeds the register file)
+    if (int rc = unit_view(s, gg, k <= 3, &uv)) return rc;
     const uint64_t maxch = 148ull * 8;
     const size_t pr = ((sizeof(double) * 2 * maxch + 255) / 256) * 256;
     if (int rc = ensure_scratch(s, pr + 16)) return rc;
@@ -1642,11 +1644,11 @@ int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, 
     if (s->dtype == DSV_C128) {
       std::vector<cplx<double>> m;
       canon_matrix<double>(gg, matrix, m);
-      CKL(launch_expect_dense(s->dtype, k, uv.g, uv.offs.data(), m.data(), s->d, d_partial, &nchunks, s->stream), 1);
+      CKL(launch_expect_dense(s->dtype, uv.mode, k, uv.g, uv.offs.data(), m.data(), s->d, d_partial, &nchunks, s->stream), 1);
     } else {
       std::vector<cplx<float>> m;
       canon_matrix<float>(gg, matrix, m);
-      CKL(launch_expect_dense(s->dtype, k, uv.g, uv.offs.data(), m.data(), s->d, d_partial, &nchunks, s->stream), 1);
+      CKL(launch_expect_dense(s->dtype, uv.mode, k, uv.g, uv.offs.data(), m.data(), s->d, d_partial, &nchunks, s->stream), 1);
     }
     prof_stop(s, t, PC_EXPECT, double(amp_bytes(s->dtype)) * double(namps(s)));
     return finish_reduce(s, 1, nchunks, 2, d_partial, d_out, out);

@@ -196,25 +196,28 @@ k_expect_dense(const __grid_constant__ DenseP<K, typename VT::R> p,
     // per-element path), one fp64 add per group
     R gr = R(0), gi = R(0);
 #pragma unroll
-    for (int r = 0; r < D; ++r) {
-      R accr = R(0), acci = R(0);
+    for (int l = 0; l < VT::L; ++l) {  // groups per unit (two with 16-byte complex64 units)
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
-        R ar, ai;
-        VT::get(in[c], 0, ar, ai);
-        const R mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
-        accr = fma(mr, ar, accr);
-        accr = fma(-mi, ai, accr);
-        acci = fma(mr, ai, acci);
-        acci = fma(mi, ar, acci);
+      for (int r = 0; r < D; ++r) {
+        R accr = R(0), acci = R(0);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          R ar, ai;
+          VT::get(in[c], l, ar, ai);
+          const R mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
+          accr = fma(mr, ar, accr);
+          accr = fma(-mi, ai, accr);
+          acci = fma(mr, ai, acci);
+          acci = fma(mi, ar, acci);
+        }
+        R xr, xi;
+        VT::get(in[r], l, xr, xi);
+        // conj(x) * acc
+        gr = fma(xr, accr, gr);
+        gr = fma(xi, acci, gr);
+        gi = fma(xr, acci, gi);
+        gi = fma(-xi, accr, gi);
       }
-      R xr, xi;
-      VT::get(in[r], 0, xr, xi);
-      // conj(x) * acc
-      gr = fma(xr, accr, gr);
-      gr = fma(xi, acci, gr);
-      gi = fma(xr, acci, gi);
-      gi = fma(-xi, accr, gi);
     }
     er += double(gr);
     ei += double(gi);
@@ -266,10 +269,19 @@ static cudaError_t expect_dense_mode(int k, const Geom& g, const uint64_t* offs,
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_expect_dense(int dtype, int k, const Geom& g, const uint64_t* offs,
+cudaError_t launch_expect_dense(int dtype, int mode, int k, const Geom& g, const uint64_t* offs,
                                 const void* matrix, const void* sv, double* d_partial,
                                 uint64_t* nchunks_out, cudaStream_t st) {
   if (dtype == 1) return expect_dense_mode<C128x1>(k, g, offs, matrix, sv, d_partial, nchunks_out, st);
+  if (mode == MODE_VEC2) {  // two groups per thread: k <= 3 (k = 4 would spill)
+    switch (k) {
+      case 0: return expect_dense_t<0, C64x2>(g, offs, matrix, sv, d_partial, nchunks_out, st);
+      case 1: return expect_dense_t<1, C64x2>(g, offs, matrix, sv, d_partial, nchunks_out, st);
+      case 2: return expect_dense_t<2, C64x2>(g, offs, matrix, sv, d_partial, nchunks_out, st);
+      case 3: return expect_dense_t<3, C64x2>(g, offs, matrix, sv, d_partial, nchunks_out, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   return expect_dense_mode<C64x1>(k, g, offs, matrix, sv, d_partial, nchunks_out, st);
 }
 

@@ -186,7 +186,7 @@ cudaError_t launch_expect_pauli(int dtype, int nbits, const PauliOp& op, const v
                                 double* d_partial, uint64_t* nchunks_out, cudaStream_t st);
 cudaError_t launch_inner(int dtype, uint64_t namps, const void* a, const void* b,
                          double* d_partial, uint64_t* nchunks_out, cudaStream_t st);
-cudaError_t launch_expect_dense(int dtype, int k, const Geom& g, const uint64_t* offs,
+cudaError_t launch_expect_dense(int dtype, int mode, int k, const Geom& g, const uint64_t* offs,
                                 const void* matrix, const void* sv, double* d_partial,
                                 uint64_t* nchunks_out, cudaStream_t st);
 // sampling: per shot, scan chunk[s] (CH amps) for the first index where the
