@@ -198,12 +198,25 @@ class DistributedStateVector:
         then needs one global<->local reorder instead of two (no data moves
         here: only the map changes)."""
         n, nloc = self.num_qubits, self.local_bits
+        ng = n - nloc
         first: dict[int, int] = {}
         for i, g in enumerate(gates):
             for q in getattr(g, "targets", ()):
                 first.setdefault(q, i)
-        order = sorted(range(n), key=lambda q: (-first.get(q, len(gates) + 1), -q))
-        glob = order[: n - nloc]
+        never = [q for q in range(n) if q not in first]
+        glob = never[:ng]
+        if len(glob) < ng:
+            # the latest gate that first-targets enough qubits takes all the
+            # remaining global slots: one reorder brings them in together
+            need = ng - len(glob)
+            for i in range(len(gates) - 1, -1, -1):
+                fresh = [q for q in getattr(gates[i], "targets", ()) if first.get(q) == i and q not in glob]
+                if len(fresh) >= need:
+                    glob += sorted(fresh)[:need]
+                    break
+        if len(glob) < ng:  # fall back: qubits whose first use as a target comes last
+            order = sorted((q for q in range(n) if q not in glob), key=lambda q: (-first.get(q, len(gates) + 1), -q))
+            glob += order[: ng - len(glob)]
         loc = [q for q in range(n) if q not in glob]
         qmap = [0] * n
         for b, q in enumerate(loc):

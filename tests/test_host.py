@@ -215,3 +215,20 @@ def test_relocation_prefers_idle_victims_and_rejects_overflow():
     assert relocation_pairs([0, 1, 2, 3], 3, [3], []) == [(3, 0)]
     with pytest.raises(InvalidArgumentError):
         relocation_pairs([0, 1, 2, 3], 2, [0, 2, 3], [])
+
+
+def test_fold_ops_stream_matches_fuse_fold():
+    """fold_ops (the generator the e2e path streams into run_circuit_sv)
+    yields exactly fuse_fold's ops, window by window."""
+    from paper_2308_01999_b200.circuits import gen_qft, gen_qv, to_gates
+    from paper_2308_01999_b200.fusion_fold import fold_ops, fuse_fold
+
+    for gates, k in ((to_gates(gen_qft(17)), 5), (to_gates(gen_qv(9, depth=6, seed=2)), 4)):
+        a = fuse_fold(gates, k).ops
+        b = list(fold_ops(gates, k))
+        assert len(a) == len(b)
+        for x, y in zip(a, b):
+            assert type(x) is type(y)
+            if hasattr(x, "matrix"):
+                assert x.targets == y.targets
+                np.testing.assert_array_equal(x.matrix, y.matrix)

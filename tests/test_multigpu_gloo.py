@@ -158,12 +158,15 @@ def _worker(rank, world, port, q):
 
         folded = fuse_fold(to_gates(gen_qft(n)), 3)
         dsv.reset()
+        before = dsv.stats.num_reorders
         dsv.run(folded.ops)
+        fold_reorders = dsv.stats.num_reorders - before
         fstate = dsv.gather_logical()
         if rank == 0:
             want = O.run_circuit(gates, n)
             fwant = O.run_circuit(to_gates(gen_qft(n)), n)
-            q.put({"fold_err": float(np.abs(fstate - fwant).max())})
+            # |0> placement: the global bits start on the qubits targeted last -> one reorder
+            q.put({"fold_err": float(np.abs(fstate - fwant).max()), "fold_reorders": fold_reorders})
             res = {
                 "state_err": float(np.abs(state - want).max()),
                 "prob_err": float(np.abs(probs - O.marginal(want, n, [6, 0, 3])).max()),
@@ -194,6 +197,7 @@ def test_distributed_protocol_over_gloo(world):
         p.join(timeout=60)
     assert "error" not in res, res
     assert fold["fold_err"] < 1e-12
+    assert fold["fold_reorders"] == 1
     assert res["state_err"] < 1e-12
     assert res["prob_err"] < 1e-12
     assert res["ev_err"] < 1e-12
