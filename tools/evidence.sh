@@ -12,3 +12,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_d
 cat gpurun_out/bench.json gpurun_out/launches.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_dense_lowt" -c 1 \
   -o gpurun_out/prof_lowt28 python tools/prof_qft_ops.py 28 5 > gpurun_out/prof_lowt28.log 2>&1
+timeout 900 python tools/sweep.py --n 33 --what targets > gpurun_out/sweep_n33.json 2> gpurun_out/sweep_n33.err
+timeout 900 python tools/ops_sweep.py > gpurun_out/ops_sweep.json 2> gpurun_out/ops_sweep.err
