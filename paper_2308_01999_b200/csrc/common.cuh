@@ -88,6 +88,13 @@ __device__ __forceinline__ void cmul_numpy(R dr, R di, R ar, R ai, R& outr, R& o
 // every amplitude is touched once per pass.
 template <typename V> __device__ __forceinline__ V ldg_s(const V* p) { return __ldcs(p); }
 template <typename V> __device__ __forceinline__ void stg_s(V* p, const V& v) { __stcs(p, v); }
+// 32-byte streaming store (sm_100: STG.256): one full sector per lane
+__device__ __forceinline__ void stcs32(void* p, float a, float b, float c, float d, float e, float f, float g,
+                                       float h) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d),
+               "f"(e), "f"(f), "f"(g), "f"(h)
+               : "memory");
+}
 
 // y = M x for one amplitude group held in registers (L lanes = groups per
 // unit), streamed out row by row.  Complex products in the 3-multiplication

@@ -281,11 +281,11 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
       tmem_ld32(tlane + uint32_t(L::T_MID + h * 32), cmid);
       tmem_ld32(tlane + uint32_t(L::T_LO + h * 32), cl);
       auto val = [&](int c) { return combine(ch[c], cmid[c], cl[c], scale, cm); };
-      if constexpr (LOWT) {
+      if constexpr (LOWT) {  // this row is contiguous: 32-byte stores, one full sector per lane
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          __stcs(reinterpret_cast<float4*>(sv + b) + h * 8 + i,
-                 make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
+        for (int i = 0; i < 4; ++i)
+          stcs32(sv + b + h * 16 + 4 * i, val(8 * i), val(8 * i + 1), val(8 * i + 2), val(8 * i + 3), val(8 * i + 4),
+                 val(8 * i + 5), val(8 * i + 6), val(8 * i + 7));
       } else if constexpr (PAIR && !PHASED) {
         // lanes 2t', 2t'+1 hold adjacent amplitudes: swap one member per pair
         // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1)
