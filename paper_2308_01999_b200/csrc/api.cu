@@ -395,6 +395,8 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   std::memset(&d, 0, sizeof d);
   d.g = uv.g;
   d.mode = tc_mode(gg);
+  // tc8 (k <= 5): index bit 0 the lowest target -> member pairs move as 16-byte units
+  if (d.mode == 0 && k <= 5 && gg.tsorted[0] == 0 && g_tc8_env) d.mode = 3;  // kTcRow2 (tcgen05.cuh)
   for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
   d.tshift = gg.tsorted[0];
   for (int m = 1; m < k; ++m)

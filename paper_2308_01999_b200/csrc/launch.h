@@ -39,7 +39,8 @@ struct TcDesc {
   int nnib_row;  // leading phase-table nibbles that vary over a tile's rows (0 when coop)
   const float* htab;  // host copy of the phase table (tile-uniform phases read it from the constant bank)
   int mode;  // 0: 8-byte copies of each thread's row, 1: index bit 0 free (16-byte row pairs),
-             // 2: targets = bits 0..k-1 (contiguous tiles, row-major staging)
+             // 2: targets = bits 0..k-1 (contiguous tiles, row-major staging),
+             // 3 (tc8 only; others treat it as 0): bit 0 the lowest target, 16-byte member pairs
   int nnib;
   int nib_shift[16];
   uint64_t offs[64];

@@ -110,6 +110,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
   using L = Tc8Layout<K>;
   constexpr bool PAIR = MODE == kTcPair;
   constexpr bool LOWT = MODE == kTcLow;
+  constexpr bool ROW2 = MODE == kTcRow2;  // stage layout [member pair m][row] x 16 B
   constexpr int D = L::D;
   constexpr int N0 = L::N0;
   constexpr int S = L::NSTAGE;
@@ -164,6 +165,10 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
           const int r = q / (D / 2), c = q % (D / 2);
           cp_async16(st0 + r * (D * 8) + ((c ^ (r & 7)) << 4), sv + tb + 2 * q);
         }
+      } else if constexpr (ROW2) {  // this row's member pairs: 16-byte copies, lanes 16 bytes apart
+        const uint64_t b = tb | rowoff;
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) cp_async16(st0 + m * 2048 + row * 16, sv + b + p.offs[2 * m]);
       } else if constexpr (PAIR) {
         const uint64_t b = tb | prowoff;
         if (p.tshift >= 0) {  // member j at j << tshift: one strided pointer
@@ -286,6 +291,11 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
         for (int i = 0; i < 4; ++i)
           stcs32(sv + b + h * 16 + 4 * i, val(8 * i), val(8 * i + 1), val(8 * i + 2), val(8 * i + 3), val(8 * i + 4),
                  val(8 * i + 5), val(8 * i + 6), val(8 * i + 7));
+      } else if constexpr (ROW2) {  // member pairs (2m, 2m+1) are adjacent amplitudes: 16-byte stores
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          __stcs(reinterpret_cast<float4*>(sv + b + p.offs[h * 16 + 2 * i]),
+                 make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
       } else if constexpr (PAIR && !PHASED) {
         // lanes 2t', 2t'+1 hold adjacent amplitudes: swap one member per pair
         // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1)
@@ -350,7 +360,14 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
     const unsigned char* stg = sm + L::RING + (grp * S + stage) * L::STAGE;
     stage = stage + 1 == S ? 0 : stage + 1;
     float2 v[D];
-    if constexpr (LOWT) {
+    if constexpr (ROW2) {
+#pragma unroll
+      for (int m = 0; m < D / 2; ++m) {
+        const float4 x = *reinterpret_cast<const float4*>(stg + m * 2048 + row * 16);
+        v[2 * m] = make_float2(x.x, x.y);
+        v[2 * m + 1] = make_float2(x.z, x.w);
+      }
+    } else if constexpr (LOWT) {
 #pragma unroll
       for (int c = 0; c < D / 2; ++c) {
         const float4 x = *reinterpret_cast<const float4*>(stg + row * (D * 8) + ((c ^ (row & 7)) << 4));
@@ -524,6 +541,7 @@ static cudaError_t tc8_k(const TcDesc& d, const void* d_bmat, const void* d_tab,
   switch (d.mode) {
     case kTcPair: return ph ? tc8_go<K, true, kTcPair>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcPair>(d, d_bmat, d_tab, sv, st);
     case kTcLow: return ph ? tc8_go<K, true, kTcLow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcLow>(d, d_bmat, d_tab, sv, st);
+    case kTcRow2: return ph ? tc8_go<K, true, kTcRow2>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcRow2>(d, d_bmat, d_tab, sv, st);
   }
   return ph ? tc8_go<K, true, kTcRow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcRow>(d, d_bmat, d_tab, sv, st);
 }

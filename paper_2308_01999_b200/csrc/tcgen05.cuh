@@ -182,6 +182,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 
 constexpr int kTcMaxNib = 10;                          // phase-table nibbles: index bits < 40
 constexpr int kTcRow = 0, kTcPair = 1, kTcLow = 2;     // tile copy modes (TcDesc::mode)
+constexpr int kTcRow2 = 3;  // tc8: index bit 0 is the lowest target: members (2m, 2m+1) move as 16-byte pairs
 constexpr float kMagic = 12582912.f;   // 1.5 * 2^23: (x + kMagic) - kMagic = rint(x), |x| < 2^22
 constexpr float kMagic16 = 49152.f;    // 1.5 * 2^15: rounds to multiples of 2^-8, |x| < 2^14
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
