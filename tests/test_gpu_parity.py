@@ -458,3 +458,23 @@ def test_expectation_and_inner_kernels(dtype):
         sv2 = sv_from(other)
         want = np.vdot(st.astype(np.complex128), other.astype(np.complex128))
         assert abs(sv.native.inner(sv2.native) - want) < tol * 4
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_sampling_multi_chunk_matches_inverse_cdf(dtype):
+    """Sampling on a state spanning many reduction chunks (2^18 amplitudes):
+    outcomes equal NumPy's inverse CDF (reference statevec.py:255-276) on the
+    same Philox variates, up to CDF-boundary ties."""
+    rng = np.random.default_rng(21)
+    n = 18
+    st = random_state(n, rng, dtype)
+    sv = sv_from(st)
+    shots = 20000
+    got = sv.sample(shots, seed=7)
+    p = np.abs(st.astype(np.complex128)) ** 2
+    cdf = np.cumsum(p / p.sum())
+    u = np.random.Generator(np.random.Philox(key=7)).random(shots)
+    idx = np.minimum(np.searchsorted(cdf, u, side="right"), (1 << n) - 1)
+    want = [format(int(i), f"0{n}b") for i in idx]
+    mism = sum(a != b for a, b in zip(got, want))
+    assert mism <= shots // 1000, mism
