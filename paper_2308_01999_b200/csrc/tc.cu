@@ -266,7 +266,7 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
 #pragma unroll
       for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
       float sn, cs;
-      sincos_red(ang, &sn, &cs);
+      sincos_unit(ang, &sn, &cs);
       Pb[(i & 1) * D + j] = make_float2(cs, sn);
     }
   };

@@ -182,7 +182,7 @@ k_dense_tc68(const __grid_constant__ Tc68P p, const uint4* __restrict__ bmat, co
 #pragma unroll
         for (int m = 0; m < 6; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
         float sn, cs;
-        sincos_red(ang, &sn, &cs);
+        sincos_unit(ang, &sn, &cs);
         Pb[j] = make_float2(cs, sn);
       }
     }

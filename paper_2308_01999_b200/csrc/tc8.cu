@@ -236,7 +236,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
 #pragma unroll
       for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
       float sn, cs;
-      sincos_red(ang, &sn, &cs);
+      sincos_unit(ang, &sn, &cs);
       Pb[(i & 1) * D + j] = make_float2(cs, sn);
     }
   };

@@ -172,6 +172,16 @@ __device__ __forceinline__ void sincos_red(float a, float* sn, float* cs) {
   const float t = a - 6.28318530717958647692f * rintf(a * 0.15915494309189533577f);
   __sincosf(t, sn, cs);
 }
+// the same, put back on the unit circle: the fast pair is off it by up to
+// ~7e-7, which the 6-7 phased passes of a QFT turn into a ~1e-6 norm drift.
+// Used where a factor is computed once per tile (cost-free), not per row.
+__device__ __forceinline__ void sincos_unit(float a, float* sn, float* cs) {
+  float s, c;
+  sincos_red(a, &s, &c);
+  const float r = rsqrtf(__fmaf_rn(s, s, c * c));
+  *sn = s * r;
+  *cs = c * r;
+}
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
