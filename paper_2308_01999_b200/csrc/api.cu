@@ -1123,11 +1123,19 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
     for (int v = 0; v < 256; ++v)
       if ((v >> bb) & 1) tab[(size_t(ci) * 256 + v) * S + t.slot] += t.th;
   }
-  const size_t es = s->dtype == DSV_C128 ? 8 : 4;
+  // unit factors exp(i angle) per (byte chunk, byte value, slot), computed in double
+  const size_t es = s->dtype == DSV_C128 ? 16 : 8;
   std::vector<unsigned char> raw(nt * es);
-  if (s->dtype == DSV_C128) std::memcpy(raw.data(), tab.data(), nt * 8);
-  else
-    for (size_t i = 0; i < nt; ++i) reinterpret_cast<float*>(raw.data())[i] = float(tab[i]);
+  for (size_t i = 0; i < nt; ++i) {
+    const double c = std::cos(tab[i]), sn = std::sin(tab[i]);
+    if (s->dtype == DSV_C128) {
+      reinterpret_cast<double*>(raw.data())[2 * i] = c;
+      reinterpret_cast<double*>(raw.data())[2 * i + 1] = sn;
+    } else {
+      reinterpret_cast<float*>(raw.data())[2 * i] = float(c);
+      reinterpret_cast<float*>(raw.data())[2 * i + 1] = float(sn);
+    }
+  }
   if (int rc = ensure_gdata(s, raw.size())) return rc;
   CK(cudaMemcpyAsync(s->gdata, raw.data(), raw.size(), cudaMemcpyHostToDevice, s->stream));
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * double(namps(s));

@@ -50,7 +50,7 @@ __device__ __forceinline__ void cmul_into(R& xr, R& xi, R er, R ei) {
 
 template <int K, class VT, bool M3>
 __global__ void __launch_bounds__(256)
-k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const typename VT::R* __restrict__ tab,
+k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const cplx<typename VT::R>* __restrict__ tab,
                typename VT::V* __restrict__ sv) {
   using V = typename VT::V;
   using R = typename VT::R;
@@ -58,7 +58,7 @@ k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const typen
   constexpr int L = VT::L;
   constexpr int S = K + 1;
   extern __shared__ __align__(16) unsigned char smem[];
-  R* st = reinterpret_cast<R*>(smem);  // [nchunk][256][S]
+  cplx<R>* st = reinterpret_cast<cplx<R>*>(smem);  // [nchunk][256][S] unit factors exp(i angle)
   const int ntab = p.nchunk * 256 * S;
   for (int i = threadIdx.x; i < ntab; i += blockDim.x) st[i] = tab[i];
   __syncthreads();
@@ -71,17 +71,25 @@ k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const typen
 #pragma unroll
     for (int l = 0; l < L; ++l) {
       const uint64_t amp = (L == 2) ? ((base << 1) | uint64_t(l)) : base;
-      R alpha[S];
+      // per-slot factors exp(i alpha_s) = product over the index bytes of the
+      // tabulated unit factors (no sin/cos per group: for complex128 the libm
+      // pair cost more than the 2^k x 2^k product)
+      R fr[S], fi[S];
+      {
+        const cplx<R>* row = st + size_t((amp >> p.chunk_shift[0]) & 255u) * S;
 #pragma unroll
-      for (int s = 0; s < S; ++s) alpha[s] = R(0);
-      for (int c = 0; c < p.nchunk; ++c) {
-        const R* row = st + (size_t(c) * 256 + ((amp >> p.chunk_shift[c]) & 255u)) * S;
+        for (int s = 0; s < S; ++s) {
+          fr[s] = row[s].x;
+          fi[s] = row[s].y;
+        }
+      }
+      for (int c = 1; c < p.nchunk; ++c) {
+        const cplx<R>* row = st + (size_t(c) * 256 + ((amp >> p.chunk_shift[c]) & 255u)) * S;
 #pragma unroll
-        for (int s = 0; s < S; ++s) alpha[s] += row[s];
+        for (int s = 0; s < S; ++s) cmul_into(fr[s], fi[s], row[s].x, row[s].y);
       }
       // P_j = exp(i gamma) * prod_{m in j} exp(i alpha_m), applied factor by factor
-      R er, ei;
-      sincos_red(alpha[K], &ei, &er);
+      R er = fr[K], ei = fi[K];
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         R ar, ai;
@@ -91,7 +99,8 @@ k_dense_phased(const __grid_constant__ PhasedP<K, typename VT::R> p, const typen
       }
 #pragma unroll
       for (int m = 0; m < K; ++m) {
-        sincos_red(alpha[m], &ei, &er);
+        er = fr[m];
+        ei = fi[m];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           if (!((j >> m) & 1)) continue;
@@ -122,7 +131,7 @@ static cudaError_t phased_go(const PhasedP<K, typename VT::R>& p, size_t smem, u
   const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return cudaSuccess;
-  k_dense_phased<K, VT, M3><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const R*>(d_tab),
+  k_dense_phased<K, VT, M3><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const cplx<R>*>(d_tab),
                                                                  static_cast<typename VT::V*>(sv));
   return cudaGetLastError();
 }
@@ -142,7 +151,7 @@ static cudaError_t phased_t(const PhasedDesc& d, const void* matrix, const void*
     p.m[i] = m[i];
     p.msum[i] = m[i].x + m[i].y;
   }
-  const size_t smem = sizeof(R) * size_t(d.nchunk) * 256 * (K + 1);
+  const size_t smem = 2 * sizeof(R) * size_t(d.nchunk) * 256 * (K + 1);
   if (use_3m()) return phased_go<K, VT, true>(p, smem, d.g.nwork, d_tab, sv, st);
   return phased_go<K, VT, false>(p, smem, d.g.nwork, d_tab, sv, st);
 }

@@ -9,9 +9,10 @@ from tools.sweep import peak
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 33
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+dt = np.complex128 if len(sys.argv) > 3 and sys.argv[3] == 'c128' else np.complex64
 pk = peak()
 ops = fuse_fold(to_gates(gen_qft(n)), k).ops
-sv = StateVector(n, dtype=np.complex64)
+sv = StateVector(n, dtype=dt)
 nat = sv.native
 res = {}
 for rep in range(3):
@@ -26,7 +27,7 @@ tot = 0.0
 for i, op in enumerate(ops):
     ms = statistics.median(m for m, _ in res[i])
     tot += ms
-    b = 16 * (1 << n)
+    b = 2 * np.dtype(dt).itemsize * (1 << n)
     tg = getattr(op, 'targets', None) or getattr(op, 'qubits', None)
     print(f"{i:2d} {type(op).__name__:16s} {str(tg):22s} {res[i][0][1]:10s} {ms:8.2f} ms  {b/ms/1e6/pk:5.2f}")
-print(f"total {tot:.1f} ms -> {577/tot*1e3 if n==33 else 0:.0f} gates/s")
+print(f"total {tot:.1f} ms -> {len(to_gates(gen_qft(n)))/tot*1e3:.0f} gates/s")
