@@ -586,8 +586,8 @@ int apply_low(dsv_state* s, const GateGeom& gg, const void* matrix, const std::v
   std::vector<cplx<float>> m;
   canon_matrix<float>(gg, matrix, m);
   ProfTok t = prof_start(s);
-  if (g_lowt_env && k == 3 && d.plain && s->nbits >= 12)
-    CKL(launch_dense_lowt(d, uint64_t(1) << s->nbits, m.data(), s->gdata, s->d, s->stream), 1);
+  if (g_lowt_env && d.plain && s->nbits >= 12)
+    CKL(launch_dense_lowt(k, d, uint64_t(1) << s->nbits, m.data(), s->gdata, s->d, s->stream), 1);
   else
     CKL(launch_dense_low(k, d, m.data(), s->gdata, s->d, s->stream), 1);
   prof_stop(s, t, prof_class, bytes);

@@ -68,9 +68,9 @@ struct LowDesc {
   int nchunk;
   int chunk_shift[8];
 };
-// k = 3, no controls, 2^n a multiple of 512: warp-transposed variant (low.cu)
-cudaError_t launch_dense_lowt(const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab, void* sv,
-                              cudaStream_t st);
+// k = 1..3, no controls, 2^n a multiple of 512: warp-transposed variant (low.cu)
+cudaError_t launch_dense_lowt(int k, const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab,
+                              void* sv, cudaStream_t st);
 cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const void* d_tab, void* sv,
                              cudaStream_t st);
 // k <= 3 (complex128) / 4 (complex64) dense gate, all targets < 6, no controls:

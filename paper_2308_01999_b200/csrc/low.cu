@@ -162,10 +162,12 @@ constexpr int kLowtRun = 512;  // amplitudes per warp run
 
 __device__ __forceinline__ uint32_t lowt_slot(uint32_t u) { return u ^ ((u >> 3) & 7u); }
 
-template <bool PHASED>
+template <int K, bool PHASED>
 __global__ void __launch_bounds__(256)
-k_dense_lowt(const __grid_constant__ LowP<3> p, uint64_t nruns, const float4* __restrict__ tab,
+k_dense_lowt(const __grid_constant__ LowP<K> p, uint64_t nruns, const float4* __restrict__ tab,
              float4* __restrict__ sv4) {
+  constexpr int D = 1 << K;
+  constexpr int G = kLowtRun / D / 32;  // groups per lane per run
   extern __shared__ float4 lsm[];  // [8 warps][256 units] run slices, then [8][256] phase slots
   float4* stab = lsm + 8 * 256;
   if constexpr (PHASED) {
@@ -196,31 +198,31 @@ k_dense_lowt(const __grid_constant__ LowP<3> p, uint64_t nruns, const float4* __
         }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int g = lane + 32 * q;  // group: amplitudes 8g .. 8g+7 of the run
-      float in[8][2];
+    for (int q = 0; q < G; ++q) {
+      const int g = lane + 32 * q;  // group: amplitudes D g .. D g + D - 1 of the run
+      float in[D][2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float4 x = slice[lowt_slot(4 * g + c)];
+      for (int c = 0; c < D / 2; ++c) {
+        const float4 x = slice[lowt_slot((D / 2) * g + c)];
         in[2 * c][0] = x.x; in[2 * c][1] = x.y; in[2 * c + 1][0] = x.z; in[2 * c + 1][1] = x.w;
       }
       if constexpr (PHASED) {
         float a[4] = {hi.x, hi.y, hi.z, hi.w};
-        const uint64_t b = rb + 8 * g;
+        const uint64_t b = rb + uint64_t(D) * g;
 #pragma unroll
         for (int c = 0; c < 2; ++c)
           if ((p.used >> c) & 1u) {
             const float4 x = stab[c * 256 + int((b >> (8 * c)) & 255u)];
             a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
           }
-        float ang[8];
-        ang[0] = a[3];
+        float ang[D];
+        ang[0] = a[K];
 #pragma unroll
-        for (int m = 0; m < 3; ++m)
+        for (int m = 0; m < K; ++m)
 #pragma unroll
           for (int j = 0; j < (1 << m); ++j) ang[j + (1 << m)] = ang[j] + a[m];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < D; ++j) {
           float sn, cs;
           sincos_low(ang[j], &sn, &cs);
           const float xr = in[j][0], xi = in[j][1];
@@ -228,13 +230,13 @@ k_dense_lowt(const __grid_constant__ LowP<3> p, uint64_t nruns, const float4* __
           in[j][1] = xr * sn + xi * cs;
         }
       }
-      float o[8][2];
+      float o[D][2];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
+      for (int r = 0; r < D; ++r) {
         float re = 0.f, im = 0.f;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float mr = p.m[r * 8 + c].x, mi = p.m[r * 8 + c].y;
+        for (int c = 0; c < D; ++c) {
+          const float mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
           re = fmaf(mr, in[c][0], re);
           re = fmaf(-mi, in[c][1], re);
           im = fmaf(mr, in[c][1], im);
@@ -244,8 +246,8 @@ k_dense_lowt(const __grid_constant__ LowP<3> p, uint64_t nruns, const float4* __
         o[r][1] = im;
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        slice[lowt_slot(4 * g + c)] = make_float4(o[2 * c][0], o[2 * c][1], o[2 * c + 1][0], o[2 * c + 1][1]);
+      for (int c = 0; c < D / 2; ++c)
+        slice[lowt_slot((D / 2) * g + c)] = make_float4(o[2 * c][0], o[2 * c][1], o[2 * c + 1][0], o[2 * c + 1][1]);
     }
     __syncwarp();
 #pragma unroll
@@ -254,10 +256,10 @@ k_dense_lowt(const __grid_constant__ LowP<3> p, uint64_t nruns, const float4* __
   }
 }
 
-template <bool PHASED>
+template <int K, bool PHASED>
 static cudaError_t lowt_go(const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab, void* sv,
                            cudaStream_t st) {
-  LowP<3> p;
+  LowP<K> p;
   std::memset(&p, 0, sizeof p);
   p.g = d.g;
   p.nchunk = d.nchunk;
@@ -270,26 +272,32 @@ static cudaError_t lowt_go(const LowDesc& d, uint64_t namps, const void* matrix,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_lowt<PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_dense_lowt<K, PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_lowt<PHASED>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_lowt<K, PHASED>, 256, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t blocks = (nruns + 7) / 8;
   const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) return cudaSuccess;
-  k_dense_lowt<PHASED><<<unsigned(blocks), 256, smem, st>>>(p, nruns, static_cast<const float4*>(d_tab),
-                                                          static_cast<float4*>(sv));
+  k_dense_lowt<K, PHASED><<<unsigned(blocks), 256, smem, st>>>(p, nruns, static_cast<const float4*>(d_tab),
+                                                             static_cast<float4*>(sv));
   return cudaGetLastError();
 }
 
-cudaError_t launch_dense_lowt(const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab, void* sv,
-                              cudaStream_t st) {
+cudaError_t launch_dense_lowt(int k, const LowDesc& d, uint64_t namps, const void* matrix, const void* d_tab,
+                              void* sv, cudaStream_t st) {
   if (!d.plain || namps % kLowtRun) return cudaErrorInvalidValue;
-  return d.nchunk > 0 ? lowt_go<true>(d, namps, matrix, d_tab, sv, st) : lowt_go<false>(d, namps, matrix, d_tab, sv, st);
+  const bool ph = d.nchunk > 0;
+  switch (k) {
+    case 1: return ph ? lowt_go<1, true>(d, namps, matrix, d_tab, sv, st) : lowt_go<1, false>(d, namps, matrix, d_tab, sv, st);
+    case 2: return ph ? lowt_go<2, true>(d, namps, matrix, d_tab, sv, st) : lowt_go<2, false>(d, namps, matrix, d_tab, sv, st);
+    case 3: return ph ? lowt_go<3, true>(d, namps, matrix, d_tab, sv, st) : lowt_go<3, false>(d, namps, matrix, d_tab, sv, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <int K, bool PHASED>
