@@ -935,13 +935,14 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   if ((k == 5 || k == 6 || (k == 4 && tc_mode(gg) == 2)) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
-  if (g_wt_env && nctrl == 0 && k >= 1 && k <= (s->dtype == DSV_C128 ? 3 : 4) && gg.tsorted[k - 1] < 6 &&
-      s->nbits >= 10) {
+  if (g_wt_env && nctrl == 0 && k >= 1 && k <= 4 && gg.tsorted[k - 1] < 6 && s->nbits >= 10) {
     // the register path strides lanes >= 32 bytes apart here: transpose through smem
     // measured weak layouts of the register path (tools/lowsweep.py, c128_bench.py):
-    // complex64 targets {1,2,3} (0.59 -> 0.95), complex128 {0,1,2} (0.60 -> 0.76)
-    const bool weak = k == 3 && (s->dtype == DSV_C128 ? gg.tsorted[0] == 0 && gg.tsorted[2] == 2
-                                                      : gg.tsorted[0] == 1 && gg.tsorted[2] == 3);
+    // complex64 targets {1,2,3} (0.59 -> 0.95), complex128 {0,1,2} (0.60 -> 0.76),
+    // complex128 k = 4 on bits 0..3
+    const bool weak = (k == 3 && (s->dtype == DSV_C128 ? gg.tsorted[0] == 0 && gg.tsorted[2] == 2
+                                                       : gg.tsorted[0] == 1 && gg.tsorted[2] == 3)) ||
+                      (k == 4 && s->dtype == DSV_C128 && gg.tsorted[3] == 3);  // bits 0..3: 0.59 -> 0.67
     if (weak) {
       ProfTok t = prof_start(s);
       if (s->dtype == DSV_C128) {

@@ -87,8 +87,9 @@ k_dense_wt(const __grid_constant__ WtP<R, K> p, R* __restrict__ sv_r) {
 template <typename R, int K>
 static cudaError_t wt_t(int nbits, const int* tb, const void* matrix, void* sv, cudaStream_t st) {
   constexpr int D = 1 << K;
-  // 8 units (128 B) per lane: 512 complex64 / 256 complex128 amplitudes per run
-  constexpr int UNITS = 256;
+  // 8 units (128 B) per lane: 512 complex64 / 256 complex128 amplitudes per run;
+  // complex128 k = 4 takes 16 units per lane (512 amplitudes: one group per lane)
+  constexpr int UNITS = (sizeof(R) == 8 && K == 4) ? 512 : 256;
   constexpr int APU = 16 / (2 * int(sizeof(R)));
   const uint64_t run_amps = uint64_t(UNITS) * APU;
   if ((uint64_t(1) << nbits) < run_amps) return cudaErrorInvalidValue;
@@ -114,7 +115,9 @@ static cudaError_t wt_t(int nbits, const int* tb, const void* matrix, void* sv, 
     p.gbase[g] = uint16_t(base);
   }
   std::memcpy(p.m, matrix, sizeof(p.m));
-  const int smem = 8 * UNITS * 16;  // 8 warps x 4 KB
+  const int smem = 8 * UNITS * 16;  // 8 warps x 4 KB (8 KB for complex128 k = 4)
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_dense_wt<R, K, UNITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_wt<R, K, UNITS>, 256, smem);
   if (per_sm < 1) per_sm = 1;
@@ -256,6 +259,7 @@ cudaError_t launch_dense_wt(int dtype, int nbits, int k, const int* tb, const vo
       case 1: return wt_t<double, 1>(nbits, tb, matrix, sv, st);
       case 2: return wt_t<double, 2>(nbits, tb, matrix, sv, st);
       case 3: return wt_t<double, 3>(nbits, tb, matrix, sv, st);
+      case 4: return wt_t<double, 4>(nbits, tb, matrix, sv, st);
     }
   } else {
     switch (k) {

@@ -332,7 +332,7 @@ def test_phased_k6_off_tensor_path_falls_back():
 def test_wt_low_targets_vs_oracle(dtype):
     rng = np.random.default_rng(31)
     n = 14
-    cases = [[1, 2, 3], [1, 3, 5], [2, 4]] if dtype == np.complex64 else [[0, 1, 2], [0, 2], [1, 2, 5]]
+    cases = [[1, 2, 3], [1, 3, 5], [2, 4]] if dtype == np.complex64 else [[0, 1, 2], [0, 2], [1, 2, 5], [0, 1, 2, 3]]
     for targets in cases:
         targets = [int(t) for t in rng.permutation(targets)]
         st = random_state(n, rng, dtype)
@@ -343,7 +343,7 @@ def test_wt_low_targets_vs_oracle(dtype):
         nat = _tc_launches(sv)
         sv.apply_matrix(G.DenseGate(m, tuple(targets)))
         prof = nat.prof_read()
-        if sorted(targets) in ([1, 2, 3], [0, 1, 2]):
+        if sorted(targets) in ([1, 2, 3], [0, 1, 2], [0, 1, 2, 3]):
             assert prof.get("dense_wt", {}).get("count", 0) == 1, prof
         tol = 2e-6 if dtype == np.complex64 else 1e-13
         assert _rel_err(sv.amplitudes, want) <= tol, (targets, prof, _rel_err(sv.amplitudes, want))
