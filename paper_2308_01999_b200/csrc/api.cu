@@ -1141,10 +1141,15 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
   CK(cudaMemcpyAsync(s->gdata, raw.data(), raw.size(), cudaMemcpyHostToDevice, s->stream));
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * double(namps(s));
   ProfTok t = prof_start(s);
+  bool lowbits = k <= 4;
+  for (int m2 = 0; m2 < k; ++m2) lowbits = lowbits && gg.tsorted[m2] == m2;
   if (s->dtype == DSV_C128) {
     std::vector<cplx<double>> m;
     canon_matrix<double>(gg, matrix, m);
-    CKL(launch_dense_phased(s->dtype, uv.mode, k, d, m.data(), s->gdata, s->d, s->stream), 1);
+    if (g_lowt_env && lowbits && s->nbits >= 12)  // warp-transposed runs: coalesced 16-byte units
+      CKL(launch_dense_lowt128(k, !terms.empty(), d, namps(s), m.data(), s->gdata, s->d, s->stream), 1);
+    else
+      CKL(launch_dense_phased(s->dtype, uv.mode, k, d, m.data(), s->gdata, s->d, s->stream), 1);
   } else {
     std::vector<cplx<float>> m;
     canon_matrix<float>(gg, matrix, m);

@@ -25,6 +25,10 @@ struct PhasedDesc {
 };
 cudaError_t launch_dense_phased(int dtype, int mode, int k, const PhasedDesc& d, const void* matrix,
                                 const void* d_tab, void* sv, cudaStream_t st);
+// complex128 k = 1..4 window on the lowest k bits (no controls), plain or with the
+// phased.cu unit-factor tables (low.cu, warp-transposed 512-amplitude runs)
+cudaError_t launch_dense_lowt128(int k, bool phased, const PhasedDesc& d, uint64_t namps, const void* matrix,
+                                 const void* d_tab, void* sv, cudaStream_t st);
 // k = 4, 5 complex64 dense gate (optionally phased) on the tensor cores
 // (tcgen05 kind::f16, exact bf16 integer limbs).  g enumerates groups in
 // amplitude space and g.nwork must be a multiple of 128; d_bmat = [limb

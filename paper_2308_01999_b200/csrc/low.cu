@@ -23,6 +23,13 @@ namespace dsv {
 constexpr int kLowItems = 4;
 
 template <int K>
+struct Low128P {
+  int nchunk;              // phase-table index bytes (0: plain dense)
+  int chunk_shift[8];
+  cplx<double> m[(1 << K) * (1 << K)];
+};
+
+template <int K>
 struct LowP {
   Geom g;                 // groups: holes = targets (bits 0..k-1) + controls
   int nchunk;             // phase-table index bytes in use (0: plain dense)
@@ -330,6 +337,168 @@ cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const 
     case 1: return ph ? low_go<1, true>(d, matrix, d_tab, sv, st) : low_go<1, false>(d, matrix, d_tab, sv, st);
     case 2: return ph ? low_go<2, true>(d, matrix, d_tab, sv, st) : low_go<2, false>(d, matrix, d_tab, sv, st);
     case 3: return ph ? low_go<3, true>(d, matrix, d_tab, sv, st) : low_go<3, false>(d, matrix, d_tab, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dsv
+
+namespace dsv {
+
+// complex128 k = 1..4 windows (plain or phased) on the lowest k bits, no
+// controls: the warp-transposed scheme of k_dense_lowt with 16-byte units of
+// one amplitude and 512-amplitude (8 KB) runs, and the phased.cu tables of
+// unit factors exp(i angle) per (index byte, value, slot) — no sin/cos per
+// group: index bytes 2.. are uniform over a run (one product per run), bytes
+// 0 and 1 vary per group.  Replaces apply_dense_bits (statevec.py:44-60) for
+// the last window of a complex128 fold-fused QFT.
+constexpr int kLowt128Run = 512;
+
+template <int K, bool PHASED>
+__global__ void __launch_bounds__(256)
+k_dense_lowt128(const __grid_constant__ Low128P<K> p, uint64_t nruns, const cplx<double>* __restrict__ tab,
+                double2* __restrict__ sv2) {
+  constexpr int D = 1 << K;
+  constexpr int S = K + 1;
+  constexpr int G = kLowt128Run / D / 32;  // groups per lane per run
+  extern __shared__ double2 lsm2[];  // [8 warps][512] run slices, then [nchunk][256][S] factors
+  cplx<double>* stab = reinterpret_cast<cplx<double>*>(lsm2 + 8 * kLowt128Run);
+  if constexpr (PHASED) {
+    for (int i = threadIdx.x; i < p.nchunk * 256 * S; i += blockDim.x) stab[i] = tab[i];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double2* slice = lsm2 + warp * kLowt128Run;
+  const uint64_t nwarps = uint64_t(gridDim.x) * 8;
+  for (uint64_t run = uint64_t(blockIdx.x) * 8 + warp; run < nruns; run += nwarps) {
+    double2* g2 = sv2 + run * kLowt128Run;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two batches of 8 loads in flight (register budget)
+      double2 t[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = __ldcs(g2 + (8 * h + i) * 32 + lane);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) slice[lowt_slot((8 * h + i) * 32 + lane)] = t[i];
+    }
+    __syncwarp();
+    const uint64_t rb = run * kLowt128Run;
+    double hr[S], hi[S];  // run-uniform factors (index bytes >= 2)
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      hr[s] = 1.0;
+      hi[s] = 0.0;
+    }
+    if constexpr (PHASED) {
+      for (int c = 0; c < p.nchunk; ++c) {
+        if (p.chunk_shift[c] < 16) continue;
+        const cplx<double>* row = stab + (size_t(c) * 256 + ((rb >> p.chunk_shift[c]) & 255u)) * S;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const double xr = hr[s] * row[s].x - hi[s] * row[s].y;
+          hi[s] = hr[s] * row[s].y + hi[s] * row[s].x;
+          hr[s] = xr;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int g = lane + 32 * q;  // group: amplitudes D g .. D g + D - 1 of the run
+      double in[D][2];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double2 x = slice[lowt_slot(D * g + j)];
+        in[j][0] = x.x;
+        in[j][1] = x.y;
+      }
+      if constexpr (PHASED) {
+        double fr[S], fi[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          fr[s] = hr[s];
+          fi[s] = hi[s];
+        }
+        const uint64_t b = rb + uint64_t(D) * g;
+        for (int c = 0; c < p.nchunk; ++c) {
+          if (p.chunk_shift[c] >= 16) continue;
+          const cplx<double>* row = stab + (size_t(c) * 256 + ((b >> p.chunk_shift[c]) & 255u)) * S;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const double xr = fr[s] * row[s].x - fi[s] * row[s].y;
+            fi[s] = fr[s] * row[s].y + fi[s] * row[s].x;
+            fr[s] = xr;
+          }
+        }
+        // member j: exp(i gamma) prod_{m in j} exp(i alpha_m)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double er = fr[K], ei = fi[K];
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            if ((j >> m) & 1) {
+              const double xr = er * fr[m] - ei * fi[m];
+              ei = er * fi[m] + ei * fr[m];
+              er = xr;
+            }
+          const double xr = in[j][0], xi = in[j][1];
+          in[j][0] = xr * er - xi * ei;
+          in[j][1] = xr * ei + xi * er;
+        }
+      }
+      // each output row goes straight back to its slot (the inputs are in registers)
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double mr = p.m[r * D + c].x, mi = p.m[r * D + c].y;
+          re = fma(mr, in[c][0], re);
+          re = fma(-mi, in[c][1], re);
+          im = fma(mr, in[c][1], im);
+          im = fma(mi, in[c][0], im);
+        }
+        slice[lowt_slot(D * g + r)] = make_double2(re, im);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) __stcs(g2 + i * 32 + lane, slice[lowt_slot(i * 32 + lane)]);
+    __syncwarp();
+  }
+}
+
+template <int K, bool PHASED>
+static cudaError_t lowt128_go(const PhasedDesc& d, uint64_t namps, const void* matrix, const void* d_tab,
+                              void* sv, cudaStream_t st) {
+  Low128P<K> p;
+  std::memset(&p, 0, sizeof p);
+  p.nchunk = PHASED ? d.nchunk : 0;
+  for (int c = 0; c < 8; ++c) p.chunk_shift[c] = d.chunk_shift[c];
+  std::memcpy(p.m, matrix, sizeof(p.m));
+  const uint64_t nruns = namps / kLowt128Run;
+  const int smem = 8 * kLowt128Run * 16 + (PHASED ? d.nchunk * 256 * (K + 1) * 16 : 0);
+  cudaError_t e = cudaFuncSetAttribute(k_dense_lowt128<K, PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_lowt128<K, PHASED>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t blocks = (nruns + 7) / 8;
+  const uint64_t cap = uint64_t(device_sm_count()) * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_lowt128<K, PHASED><<<unsigned(blocks), 256, smem, st>>>(p, nruns, static_cast<const cplx<double>*>(d_tab),
+                                                                 static_cast<double2*>(sv));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_lowt128(int k, bool phased, const PhasedDesc& d, uint64_t namps, const void* matrix,
+                                 const void* d_tab, void* sv, cudaStream_t st) {
+  if (namps % kLowt128Run) return cudaErrorInvalidValue;
+  switch (k) {
+    case 1: return phased ? lowt128_go<1, true>(d, namps, matrix, d_tab, sv, st) : lowt128_go<1, false>(d, namps, matrix, d_tab, sv, st);
+    case 2: return phased ? lowt128_go<2, true>(d, namps, matrix, d_tab, sv, st) : lowt128_go<2, false>(d, namps, matrix, d_tab, sv, st);
+    case 3: return phased ? lowt128_go<3, true>(d, namps, matrix, d_tab, sv, st) : lowt128_go<3, false>(d, namps, matrix, d_tab, sv, st);
+    case 4: return phased ? lowt128_go<4, true>(d, namps, matrix, d_tab, sv, st) : lowt128_go<4, false>(d, namps, matrix, d_tab, sv, st);
   }
   return cudaErrorInvalidValue;
 }

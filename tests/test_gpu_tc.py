@@ -254,6 +254,31 @@ def test_low_phased_vs_oracle(k):
         assert _rel_err(sv.amplitudes, want) <= 2 * REL, (trial, _rel_err(sv.amplitudes, want))
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_low_phased_complex128_vs_oracle(k):
+    """complex128 windows on the lowest k bits (warp-transposed runs with the
+    unit-factor phase tables), plain and phased, against the oracle."""
+    rng = np.random.default_rng(1750 + k)
+    for trial in range(3):
+        n = int(rng.integers(12, 17))
+        targets = list(range(k))
+        outside_bits = list(range(k, n))
+        if trial == 0:
+            cross, outside = [], []
+        else:
+            cross = [(int(rng.integers(0, k)), int(b), float(rng.uniform(-7, 7)))
+                     for b in rng.choice(outside_bits, size=min(12, len(outside_bits)), replace=False)]
+            outside = [(int(b), float(rng.uniform(-7, 7))) for b in rng.choice(outside_bits, size=4, replace=False)]
+        st = random_state(n, rng, np.complex128)
+        m = G.random_unitary(1 << k, rng)
+        want = st * np.exp(1j * _phase_angles(n, targets, cross, outside))
+        O.apply_dense(want, n, m, targets, [])
+        sv = StateVector.from_amplitudes(st)
+        sv.native.apply_matrix_phased(m, targets, cross, outside)
+        sv._mutated()
+        assert _rel_err(sv.amplitudes, want) <= 1e-12, (trial, _rel_err(sv.amplitudes, want))
+
+
 # ---- k = 6 windows (tc6.cu) -------------------------------------------------------------------
 
 @pytest.mark.parametrize("case", ["high", "mid", "spread", "bit0", "ctrl"])
