@@ -1202,6 +1202,36 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
   bool is_diag = true;
   for (uint64_t j = 0; j < D; ++j) is_diag = is_diag && pn[j] == j;
   const int kk = k + nctrl;
+  if (is_diag && nactive == 1 && s->dtype == DSV_C64 && !(!gg.holes.empty() && gg.holes[0] == 0) &&
+      s->nbits >= 1) {
+    // one non-unit entry (controlled phase, CZ, T on a control subcube ...):
+    // every target and control bit is fixed, so enumerate exactly the
+    // amplitudes it scales (holes = targets + controls, forced to the entry's
+    // bits) and multiply in contiguous 16-byte runs; no table, no skipped work
+    uint64_t ja = 0;
+    for (uint64_t j = 0; j < D; ++j)
+      if (act[j]) ja = j;
+    uint64_t forced = gg.set_mask;  // control values (amp space)
+    for (int m = 0; m < k; ++m)
+      if ((ja >> m) & 1) forced |= 1ull << gg.tsorted[m];
+    // (complex64 with bit 0 free only: 16-byte units; with bit 0 fixed the
+    // affected amplitudes sit 16 bytes apart and the sector-skipping stream
+    // kernel below is faster)
+    const bool vec2 = true;
+    const int sh = 1;
+    std::vector<int> h(gg.holes);
+    for (int& x : h) x -= sh;
+    Geom geo;
+    if (int rc = make_geom(s->nbits - sh, h, forced >> sh, &geo)) return rc;
+    const size_t es = amp_bytes(s->dtype);
+    std::vector<unsigned char> d1(es);
+    std::memcpy(d1.data(), dn.data() + ja * es, es);
+    const unsigned char one = 1;
+    ProfTok t = prof_start(s);
+    CKL(launch_diag(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, 0, geo, nullptr, d1.data(), &one, s->d, s->stream), 1);
+    prof_stop(s, t, PC_DIAG, bytes);
+    return DSV_OK;
+  }
   if (is_diag && kk <= (s->dtype == DSV_C64 ? kDiagStreamMaxBits : kDiagStreamMaxBits - 1)) {
     // streaming path: one table over targets + controls, contiguous 16-B units
     std::vector<int> B(gg.holes);  // sorted targets + controls (amp bits)

@@ -198,7 +198,7 @@ static cudaError_t diag_t(const Geom& g, int k, const int* tb, const void* diag,
   DiagP<R> p;
   p.g = g;
   p.k = k;
-  for (int m = 0; m < DSV_MAX_TARGETS_; ++m) p.tb[m] = m < k ? tb[m] : 0;
+  for (int m = 0; m < DSV_MAX_TARGETS_; ++m) p.tb[m] = (m < k && tb) ? tb[m] : 0;
   const cplx<R>* d = static_cast<const cplx<R>*>(diag);
   for (int j = 0; j < (1 << k); ++j) {
     p.d[j] = d[j];

@@ -478,3 +478,24 @@ def test_sampling_multi_chunk_matches_inverse_cdf(dtype):
     want = [format(int(i), f"0{n}b") for i in idx]
     mism = sum(a != b for a, b in zip(got, want))
     assert mism <= shots // 1000, mism
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_single_entry_diagonals_bit_exact(dtype):
+    """Diagonals with one non-unit entry (CP, CZ, controlled T, ...) take the
+    enumerate-only-the-affected-amplitudes path: bit-exact vs the oracle,
+    including bit 0 as target or control."""
+    rng = np.random.default_rng(404)
+    n = 12
+    cases = [((3,), [(4, 1)]), ((0,), [(1, 1)]), ((11,), [(0, 1)]), ((2, 7), [(5, 0)]), ((0, 1), []),
+             ((6,), [(0, 1), (9, 0)])]
+    for targets, ctrls in cases:
+        k = len(targets)
+        st = random_state(n, rng, dtype)
+        diag = np.ones(1 << k, dtype=np.complex128)
+        diag[int(rng.integers(0, 1 << k))] = np.exp(1j * rng.uniform(0, 2 * np.pi))
+        want = st.copy()
+        O.apply_genperm(want, n, np.arange(1 << k), diag, list(targets), ctrls)
+        sv = sv_from(st)
+        sv.apply_generalized_permutation(G.PermutationGate(np.arange(1 << k), diag, targets, tuple(ctrls)))
+        _check(sv.amplitudes, want, dtype, exact=True)
