@@ -1309,6 +1309,37 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
     prof_stop(s, t, PC_PERM, bytes);
     return DSV_OK;
   }
+  // complex64, index bit 0 a control (e.g. CNOT controlled by qubit 0): the
+  // affected amplitudes sit 16 bytes apart; move whole 16-byte units over the
+  // other bits and let only the control's lane change (full sectors instead of
+  // half-used ones)
+  int ctl0 = -1;
+  for (int c = 0; c < nctrl; ++c)
+    if (cb[c] == 0) ctl0 = cv[c];
+  if (ctl0 >= 0 && s->dtype == DSV_C64 && k >= 1 && k <= 4 && s->nbits >= 2) {
+    std::vector<int> h;
+    for (int b : gg.holes)
+      if (b != 0) h.push_back(b - 1);
+    Geom geo;
+    if (int rc = make_geom(s->nbits - 1, h, (gg.set_mask & ~1ull) >> 1, &geo)) return rc;
+    std::vector<uint64_t> oi(D), oo(D);
+    std::vector<uint8_t> pd(D);
+    for (uint64_t j = 0; j < D; ++j) {
+      uint64_t o = 0;
+      for (int m = 0; m < k; ++m) o |= ((j >> m) & 1ull) << (gg.tsorted[m] - 1);
+      oi[j] = o;
+    }
+    uint64_t active = 0;
+    for (uint64_t j = 0; j < D; ++j) {
+      oo[j] = oi[pn[j]];
+      pd[j] = uint8_t(pn[j]);
+      if (act[j]) active |= 1ull << j;
+    }
+    ProfTok t = prof_start(s);
+    CKL(launch_perm_lanectl(k, geo, oi.data(), oo.data(), dn.data(), active, ctl0, pd.data(), s->d, s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
   if (k <= kPermRegMaxK) {
     UnitView uv;
     if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;

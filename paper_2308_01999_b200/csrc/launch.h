@@ -113,6 +113,12 @@ cudaError_t launch_diag_stream(int dtype, int nbits, int kk, const int* amp_bits
 cudaError_t launch_perm_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs_in,
                             const uint64_t* offs_out, const void* diag, uint64_t active,
                             void* sv, cudaStream_t st);
+// complex64 permutation whose index bit 0 is a CONTROL: 16-byte units over the
+// other bits, only lane `lanectl` (the control value) of each unit moves; the
+// destination unit's other lane keeps its value (pdst[j] = perm[j])
+cudaError_t launch_perm_lanectl(int k, const Geom& g, const uint64_t* offs_in, const uint64_t* offs_out,
+                                const void* diag, uint64_t active, int lanectl, const uint8_t* pdst, void* sv,
+                                cudaStream_t st);
 cudaError_t launch_perm_generic(int dtype, int k, const Geom& g, const uint64_t* d_offs_in,
                                 const uint64_t* d_offs_out, const void* d_diag, void* sv,
                                 cudaStream_t st);

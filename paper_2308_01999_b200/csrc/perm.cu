@@ -22,9 +22,11 @@ template <int K, typename R>
 struct PermP {
   Geom g;
   int cached;       // members share 128-byte lines (low targets): L1-cached loads
+  int lanectl;      // 16-byte units with index bit 0 a CONTROL: only lane (bit 0 value) lanectl moves, else -1
   uint64_t active;  // bit j set: entry j moves or scales
   uint64_t offs_in[1 << K];
   uint64_t offs_out[1 << K];  // offs[perm[j]]
+  uint8_t pdst[1 << K];       // perm[j] (lanectl: the destination's other lane keeps its own value)
   cplx<R> d[1 << K];
 };
 
@@ -67,8 +69,14 @@ k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __res
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         R ar, ai, orr, oi;
-        VT::get(in[it][j], l, ar, ai);
-        cmul_numpy(dr, di, ar, ai, orr, oi);
+        if (L == 2 && p.lanectl >= 0 && l != p.lanectl) {  // control not met: the destination keeps its lane
+#pragma unroll
+          for (int q = 0; q < D; ++q)
+            if (q == p.pdst[j]) VT::get(in[it][q], l, orr, oi);
+        } else {
+          VT::get(in[it][j], l, ar, ai);
+          cmul_numpy(dr, di, ar, ai, orr, oi);
+        }
         VT::set(out, l, orr, oi);
       }
       stg_s(sv + base[it] + p.offs_out[j], out);
@@ -78,13 +86,16 @@ k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __res
 
 template <int K, class VT>
 static cudaError_t perm_reg_t(const Geom& g, const uint64_t* offs_in, const uint64_t* offs_out,
-                              const void* diag, uint64_t active, void* sv, cudaStream_t st) {
+                              const void* diag, uint64_t active, void* sv, cudaStream_t st,
+                              int lanectl = -1, const uint8_t* pdst = nullptr) {
   using R = typename VT::R;
   constexpr int D = 1 << K;
   constexpr int ITEMS = PermItems<VT, K>::value;
   PermP<K, R> p;
   p.g = g;
   p.active = active;
+  p.lanectl = lanectl;
+  for (int j = 0; j < D; ++j) p.pdst[j] = pdst ? pdst[j] : uint8_t(j);
   uint64_t span = 0;
   for (int j = 0; j < D; ++j) span |= offs_in[j];
   p.cached = span != 0 && span * sizeof(typename VT::V) < 256;
@@ -103,16 +114,23 @@ static cudaError_t perm_reg_t(const Geom& g, const uint64_t* offs_in, const uint
 
 template <class VT>
 static cudaError_t perm_reg_mode(int k, const Geom& g, const uint64_t* oi, const uint64_t* oo,
-                                 const void* d, uint64_t a, void* sv, cudaStream_t st) {
+                                 const void* d, uint64_t a, void* sv, cudaStream_t st, int lanectl = -1,
+                                 const uint8_t* pdst = nullptr) {
   switch (k) {
-    case 0: return perm_reg_t<0, VT>(g, oi, oo, d, a, sv, st);
-    case 1: return perm_reg_t<1, VT>(g, oi, oo, d, a, sv, st);
-    case 2: return perm_reg_t<2, VT>(g, oi, oo, d, a, sv, st);
-    case 3: return perm_reg_t<3, VT>(g, oi, oo, d, a, sv, st);
-    case 4: return perm_reg_t<4, VT>(g, oi, oo, d, a, sv, st);
-    case 5: return perm_reg_t<5, VT>(g, oi, oo, d, a, sv, st);
+    case 0: return perm_reg_t<0, VT>(g, oi, oo, d, a, sv, st, lanectl, pdst);
+    case 1: return perm_reg_t<1, VT>(g, oi, oo, d, a, sv, st, lanectl, pdst);
+    case 2: return perm_reg_t<2, VT>(g, oi, oo, d, a, sv, st, lanectl, pdst);
+    case 3: return perm_reg_t<3, VT>(g, oi, oo, d, a, sv, st, lanectl, pdst);
+    case 4: return perm_reg_t<4, VT>(g, oi, oo, d, a, sv, st, lanectl, pdst);
+    case 5: return perm_reg_t<5, VT>(g, oi, oo, d, a, sv, st, lanectl, pdst);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_perm_lanectl(int k, const Geom& g, const uint64_t* offs_in, const uint64_t* offs_out,
+                                const void* diag, uint64_t active, int lanectl, const uint8_t* pdst, void* sv,
+                                cudaStream_t st) {
+  return perm_reg_mode<C64x2>(k, g, offs_in, offs_out, diag, active, sv, st, lanectl, pdst);
 }
 
 cudaError_t launch_perm_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs_in,

@@ -499,3 +499,24 @@ def test_single_entry_diagonals_bit_exact(dtype):
         sv = sv_from(st)
         sv.apply_generalized_permutation(G.PermutationGate(np.arange(1 << k), diag, targets, tuple(ctrls)))
         _check(sv.amplitudes, want, dtype, exact=True)
+
+
+@pytest.mark.parametrize("ctl_val", [0, 1])
+def test_permutations_controlled_by_bit0_bit_exact(ctl_val):
+    """complex64 permutations with index bit 0 as a control (CX(0, t), ...):
+    16-byte units where only the control's lane moves; bit-exact vs oracle."""
+    rng = np.random.default_rng(505 + ctl_val)
+    n = 12
+    for targets, extra in (((11,), []), ((3,), []), ((1,), []), ((2, 9), [(5, 1)]), ((4, 6, 7), []),
+                           ((1, 2, 3, 8), [(11, 0)])):
+        k = len(targets)
+        st = random_state(n, rng, np.complex64)
+        perm = rng.permutation(1 << k)
+        diag = np.exp(1j * rng.uniform(0, 2 * np.pi, 1 << k))
+        diag[rng.random(1 << k) < 0.3] = 1.0
+        ctrls = [(0, ctl_val)] + extra
+        want = st.copy()
+        O.apply_genperm(want, n, perm, diag, list(targets), ctrls)
+        sv = sv_from(st)
+        sv.apply_generalized_permutation(G.PermutationGate(perm, diag, targets, tuple(ctrls)))
+        _check(sv.amplitudes, want, np.complex64, exact=True)

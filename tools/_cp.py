@@ -14,3 +14,10 @@ for t, c in ((3, 4), (17, 18), (32, 0), (0, 1), (20, 5)):
         nat.event_record(0); sv.apply(op); nat.event_record(1); ts.append(nat.event_elapsed(0, 1))
     ms = statistics.median(ts[1:])
     print("cp", t, c, f"{ms:.2f} ms {8*2*(1<<n)/4/ms/1e6/pk:.2f}", flush=True)
+for t, c in ((32, 0), (5, 0), (17, 0)):
+    op = G.cx(c, t)
+    ts = []
+    for _ in range(4):
+        nat.event_record(0); sv.apply(op); nat.event_record(1); ts.append(nat.event_elapsed(0, 1))
+    ms = statistics.median(ts[1:])
+    print("cx", t, c, f"{ms:.2f} ms alg {8*2*(1<<n)/2/ms/1e6/pk:.2f}", flush=True)
