@@ -1441,6 +1441,13 @@ int dsv_swap_index_bits(dsv_state* s, const int32_t* pairs, int npairs) {
   }
   if (sp.np == 0) return DSV_OK;
   DeviceGuard g(s->device);
+  if (sp.np == 1 && bit0 && s->dtype == DSV_C64 && s->nbits >= 2) {
+    const int b = sp.a[0] == 0 ? sp.b[0] : sp.a[0];
+    ProfTok t = prof_start(s);
+    CKL(launch_swap_bit0(s->nbits, b, s->d, s->stream), 1);
+    prof_stop(s, t, PC_SWAP, double(amp_bytes(s->dtype)) * double(namps(s)));
+    return DSV_OK;
+  }
   int mode = MODE_SCALAR;
   uint64_t nunits = namps(s);
   if (s->dtype == DSV_C64 && !bit0) {

@@ -137,6 +137,8 @@ struct SwapGeomP {
   int nsw;
   uint64_t oi[28], oj[28];
 };
+// complex64 swap of index bit 0 with bit b (one pair): half-unit exchange of 16-byte units (layout.cu)
+cudaError_t launch_swap_bit0(int nbits, int b, void* sv, cudaStream_t st);
 cudaError_t launch_swap_geom(int dtype, int mode, const SwapGeomP& p, void* sv, cudaStream_t st);
 cudaError_t launch_gather(int dtype, int nbits, const int32_t* ordering, uint64_t begin,
                           uint64_t count, const void* sv, void* d_out, cudaStream_t st);

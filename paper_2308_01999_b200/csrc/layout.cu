@@ -5,6 +5,8 @@
 //     as a one-pass in-place swap over peer-visible pointers)
 //   * collapse / scale               (measure's collapse, statevec.py:229-237)
 //   * Pauli rotation / product        (statevec.py:84-104, :196-207, copy-free)
+#include <cstring>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -92,6 +94,57 @@ cudaError_t launch_swap_geom(int dtype, int mode, const SwapGeomP& p, void* sv, 
   if (dtype == 1) return swap_geom_mode<C128x1>(p, sv, st);
   if (mode == MODE_VEC2) return swap_geom_mode<C64x2>(p, sv, st);
   return swap_geom_mode<C64x1>(p, sv, st);
+}
+
+// complex64 swap of index bit 0 with bit b: in 16-byte units (amplitudes
+// 2u, 2u+1) the pair exchanges the odd half of unit u (unit bit b-1 = 0)
+// with the even half of unit u | 2^(b-1); whole units move, so every sector is
+// read and written once in full (the scalar path's 8-byte accesses used half
+// of each sector per instruction).
+__global__ void __launch_bounds__(256)
+k_swap_bit0(float4* __restrict__ sv, const __grid_constant__ Geom g, uint64_t partner) {
+  constexpr int ITEMS = 4;
+  const uint64_t w0 = uint64_t(blockIdx.x) * (256ull * ITEMS) + threadIdx.x;
+  float4 x[ITEMS], y[ITEMS];
+  uint64_t u[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * 256;
+    u[it] = expand(g, w);
+    if (w < g.nwork) {
+      x[it] = ldg_s(sv + u[it]);
+      y[it] = ldg_s(sv + (u[it] | partner));
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t w = w0 + uint64_t(it) * 256;
+    if (w >= g.nwork) continue;
+    stg_s(sv + u[it], make_float4(x[it].x, x[it].y, y[it].x, y[it].y));
+    stg_s(sv + (u[it] | partner), make_float4(x[it].z, x[it].w, y[it].z, y[it].w));
+  }
+}
+
+cudaError_t launch_swap_bit0(int nbits, int b, void* sv, cudaStream_t st) {
+  if (b < 1 || b >= nbits) return cudaErrorInvalidValue;
+  Geom g;
+  std::memset(&g, 0, sizeof g);
+  // unit space (nbits - 1 bits) with unit bit b - 1 a hole
+  const int ubits = nbits - 1, h = b - 1;
+  g.nwork = 1ull << (ubits - 1);
+  g.set_mask = 0;
+  g.nseg = 0;
+  const uint64_t lo = (1ull << h) - 1ull;
+  if (lo) {
+    g.seg[g.nseg] = lo;
+    g.shift[g.nseg++] = 0;
+  }
+  g.seg[g.nseg] = ~((1ull << (h + 1)) - 1ull);
+  g.shift[g.nseg++] = 1;
+  const uint64_t blocks = (g.nwork + 1023) / 1024;
+  if (blocks == 0) return cudaSuccess;
+  k_swap_bit0<<<unsigned(blocks), 256, 0, st>>>(static_cast<float4*>(sv), g, 1ull << h);
+  return cudaGetLastError();
 }
 
 static unsigned grid_for(uint64_t n, int per_thread = 1) {
