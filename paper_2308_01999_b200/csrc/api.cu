@@ -1010,6 +1010,32 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
     prof_stop(s, t, PC_DENSE_TILE, bytes);
     return DSV_OK;
   }
+  {
+    // complex64 with index bit 0 a control: whole 16-byte units, only the
+    // control's lane transformed (the scalar path uses half of every sector)
+    int ctl0 = -1;
+    for (int c = 0; c < nctrl; ++c)
+      if (cb[c] == 0) ctl0 = cv[c];
+    if (ctl0 >= 0 && s->dtype == DSV_C64 && k >= 1 && k <= 4 && s->nbits >= 2) {
+      std::vector<int> h;
+      for (int b : gg.holes)
+        if (b != 0) h.push_back(b - 1);
+      Geom geo;
+      if (int rc = make_geom(s->nbits - 1, h, (gg.set_mask & ~1ull) >> 1, &geo)) return rc;
+      std::vector<uint64_t> offs(D);
+      for (uint64_t j = 0; j < D; ++j) {
+        uint64_t o = 0;
+        for (int m = 0; m < k; ++m) o |= ((j >> m) & 1ull) << (gg.tsorted[m] - 1);
+        offs[j] = o;
+      }
+      std::vector<cplx<float>> m;
+      canon_matrix<float>(gg, matrix, m);
+      ProfTok t = prof_start(s);
+      CKL(launch_dense_lanectl(k, geo, offs.data(), m.data(), ctl0, s->d, s->stream), 1);
+      prof_stop(s, t, PC_DENSE, bytes);
+      return DSV_OK;
+    }
+  }
   if (k <= kDenseRegMaxK) {
     UnitView uv;
     // float4 pairs only while 2^k x 2 amplitudes fit the register budget

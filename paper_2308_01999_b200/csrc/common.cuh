@@ -106,7 +106,7 @@ template <int D, class VT>
 __device__ __forceinline__ void matvec3m_store(const cplx<typename VT::R>* __restrict__ m,
                                                const typename VT::R* __restrict__ msum,
                                                const typename VT::V (&in)[D], typename VT::V* sv,
-                                               uint64_t base, const uint64_t* offs) {
+                                               uint64_t base, const uint64_t* offs, int lanectl = -1) {
   using R = typename VT::R;
   using V = typename VT::V;
   constexpr int L = VT::L;
@@ -136,6 +136,11 @@ __device__ __forceinline__ void matvec3m_store(const cplx<typename VT::R>* __res
     V out;
 #pragma unroll
     for (int l = 0; l < L; ++l) VT::set(out, l, P[l] - Q[l], S[l] - P[l] - Q[l]);
+    if (L == 2 && lanectl >= 0) {  // control on index bit 0 not met: that lane keeps its input
+      R xr, xi;
+      VT::get(in[r], 1 - lanectl, xr, xi);
+      VT::set(out, 1 - lanectl, xr, xi);
+    }
     __stcs(sv + base + offs[r], out);
   }
 }
@@ -144,7 +149,7 @@ __device__ __forceinline__ void matvec3m_store(const cplx<typename VT::R>* __res
 template <int D, class VT>
 __device__ __forceinline__ void matvec4m_store(const cplx<typename VT::R>* __restrict__ m,
                                                const typename VT::V (&in)[D], typename VT::V* sv,
-                                               uint64_t base, const uint64_t* offs) {
+                                               uint64_t base, const uint64_t* offs, int lanectl = -1) {
   using R = typename VT::R;
   using V = typename VT::V;
   constexpr int L = VT::L;

@@ -18,6 +18,7 @@ template <int K, typename R>
 struct DenseP {
   Geom g;
   int cached;  // members share 128-byte lines (low targets): L1-cached loads, not streaming
+  int lanectl;  // 16-byte units with index bit 0 a CONTROL: only lane lanectl is transformed, else -1
   uint64_t offs[1 << K];
   cplx<R> m[(1 << K) * (1 << K)];
   R msum[(1 << K) * (1 << K)];  // re + im of m (3-multiplication products)
@@ -54,7 +55,7 @@ k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __r
     const uint64_t w = w0 + uint64_t(it) * blockDim.x;
     if (w >= p.g.nwork) continue;
     if constexpr (M3) {  // FMA-bound regime: 3-multiplication complex products
-      matvec3m_store<D, VT>(p.m, p.msum, in[it], sv, base[it], p.offs);
+      matvec3m_store<D, VT>(p.m, p.msum, in[it], sv, base[it], p.offs, p.lanectl);
       continue;
     }
 #pragma unroll
@@ -78,6 +79,11 @@ k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __r
       V out;
 #pragma unroll
       for (int l = 0; l < L; ++l) VT::set(out, l, accr[l], acci[l]);
+      if (L == 2 && p.lanectl >= 0) {  // control on index bit 0 not met: that lane keeps its input
+        R xr, xi;
+        VT::get(in[it][r], 1 - p.lanectl, xr, xi);
+        VT::set(out, 1 - p.lanectl, xr, xi);
+      }
       stg_s(sv + base[it] + p.offs[r], out);
     }
   }
@@ -85,12 +91,13 @@ k_dense(const __grid_constant__ DenseP<K, typename VT::R> p, typename VT::V* __r
 
 template <int K, class VT>
 static cudaError_t dense_reg_t(const Geom& g, const uint64_t* offs, const void* matrix, void* sv,
-                               cudaStream_t st) {
+                               cudaStream_t st, int lanectl = -1) {
   using R = typename VT::R;
   constexpr int D = 1 << K;
   constexpr int ITEMS = DenseItems<VT, K>::value;
   DenseP<K, R> p;
   p.g = g;
+  p.lanectl = lanectl;
   uint64_t span = 0;
   for (int j = 0; j < D; ++j) {
     p.offs[j] = offs[j];
@@ -122,6 +129,17 @@ static cudaError_t dense_reg_mode(int k, const Geom& g, const uint64_t* offs, co
     case 3: return dense_reg_t<3, VT>(g, offs, m, sv, st);
     case 4: return dense_reg_t<4, VT>(g, offs, m, sv, st);
     case 5: return dense_reg_t<5, VT>(g, offs, m, sv, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_dense_lanectl(int k, const Geom& g, const uint64_t* offs, const void* matrix, int lanectl,
+                                 void* sv, cudaStream_t st) {
+  switch (k) {
+    case 1: return dense_reg_t<1, C64x2>(g, offs, matrix, sv, st, lanectl);
+    case 2: return dense_reg_t<2, C64x2>(g, offs, matrix, sv, st, lanectl);
+    case 3: return dense_reg_t<3, C64x2>(g, offs, matrix, sv, st, lanectl);
+    case 4: return dense_reg_t<4, C64x2>(g, offs, matrix, sv, st, lanectl);
   }
   return cudaErrorInvalidValue;
 }

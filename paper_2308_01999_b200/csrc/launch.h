@@ -13,6 +13,9 @@ enum Mode { MODE_SCALAR = 0, MODE_VEC2 = 1 };  // VEC2: complex64 with index bit
 // dense k-qubit gate, k <= 5, matrix (canonical sorted-target order, state real
 // type, row-major) passed by value in the kernel parameter block
 constexpr int kDenseRegMaxK = 5;
+// complex64 dense k <= 4 with index bit 0 a CONTROL: 16-byte units over the other bits, lane lanectl transformed
+cudaError_t launch_dense_lanectl(int k, const Geom& g, const uint64_t* offs, const void* matrix, int lanectl,
+                                 void* sv, cudaStream_t st);
 cudaError_t launch_dense_reg(int dtype, int mode, int k, const Geom& g, const uint64_t* offs,
                              const void* matrix, void* sv, cudaStream_t st);
 // k <= 5 dense gate preceded by an outside-coupled phase polynomial

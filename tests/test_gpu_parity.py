@@ -520,3 +520,21 @@ def test_permutations_controlled_by_bit0_bit_exact(ctl_val):
         sv = sv_from(st)
         sv.apply_generalized_permutation(G.PermutationGate(perm, diag, targets, tuple(ctrls)))
         _check(sv.amplitudes, want, np.complex64, exact=True)
+
+
+@pytest.mark.parametrize("ctl_val", [0, 1])
+def test_dense_controlled_by_bit0(ctl_val):
+    """complex64 dense gates with index bit 0 as a control: 16-byte units,
+    only the control lane transformed; vs the oracle (fp32 tolerance)."""
+    rng = np.random.default_rng(606 + ctl_val)
+    n = 12
+    for targets, extra in (((11,), []), ((1,), []), ((3, 8), []), ((2, 5, 9), [(7, 1)]), ((1, 2, 3, 4), [])):
+        k = len(targets)
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng)
+        ctrls = [(0, ctl_val)] + extra
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), list(targets), ctrls)
+        sv = sv_from(st)
+        sv.apply_matrix(G.DenseGate(m, targets, tuple(ctrls)))
+        assert np.abs(sv.amplitudes - want).max() <= 1e-5 * np.abs(want).max() * 4
