@@ -1228,6 +1228,30 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
   bool is_diag = true;
   for (uint64_t j = 0; j < D; ++j) is_diag = is_diag && pn[j] == j;
   const int kk = k + nctrl;
+  if (is_diag && nactive == 1 && s->dtype == DSV_C64 && s->nbits >= 2 && !gg.holes.empty() && gg.holes[0] == 0 &&
+      (gg.holes.size() < 2 || gg.holes[1] >= 2)) {  // (bit 1 fixed too: units 32 B apart, the stream kernel wins)
+    // the same with index bit 0 fixed (target or control): 16-byte units over
+    // the other bits, only the lane with bit 0's value is scaled
+    uint64_t ja = 0;
+    for (uint64_t j = 0; j < D; ++j)
+      if (act[j]) ja = j;
+    uint64_t forced = gg.set_mask;
+    for (int m = 0; m < k; ++m)
+      if ((ja >> m) & 1) forced |= 1ull << gg.tsorted[m];
+    const int lane = int(forced & 1ull);
+    std::vector<int> h;
+    for (int b : gg.holes)
+      if (b != 0) h.push_back(b - 1);
+    Geom geo;
+    if (int rc = make_geom(s->nbits - 1, h, (forced & ~1ull) >> 1, &geo)) return rc;
+    const size_t es = amp_bytes(s->dtype);
+    std::vector<unsigned char> d1(es);
+    std::memcpy(d1.data(), dn.data() + ja * es, es);
+    ProfTok t = prof_start(s);
+    CKL(launch_diag_lane(geo, d1.data(), lane, s->d, s->stream), 1);
+    prof_stop(s, t, PC_DIAG, bytes);
+    return DSV_OK;
+  }
   if (is_diag && nactive == 1 && s->dtype == DSV_C64 && !(!gg.holes.empty() && gg.holes[0] == 0) &&
       s->nbits >= 1) {
     // one non-unit entry (controlled phase, CZ, T on a control subcube ...):

@@ -105,6 +105,8 @@ cudaError_t launch_dense_generic(int dtype, int k, const Geom& g, const uint64_t
 constexpr int kPermRegMaxK = 5;
 // diagonal (identity permutation), any k <= 10: elementwise streaming;
 // tb = unit-space target bits (sorted), active[j] = entry j differs from 1
+// complex64 single-entry diagonal over 16-byte units: scale lane lanectl (bit 0 value) of every enumerated unit
+cudaError_t launch_diag_lane(const Geom& g, const void* diag, int lanectl, void* sv, cudaStream_t st);
 cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb, const void* diag,
                         const unsigned char* active, void* sv, cudaStream_t st);
 // streaming diagonal over a table of kk <= kDiagStreamMaxBits bits (targets and

@@ -154,6 +154,7 @@ template <typename R>
 struct DiagP {
   Geom g;                 // holes = controls, unit space
   int k;
+  int lanectl;            // 16-byte units: only lane lanectl (index bit 0 value) is scaled, else -1
   int tb[DSV_MAX_TARGETS_];  // unit-space target bits, sorted
   cplx<R> d[1 << DSV_MAX_TARGETS_];
   unsigned char active[1 << DSV_MAX_TARGETS_];
@@ -198,6 +199,7 @@ k_diag(const __grid_constant__ DiagP<typename VT::R> p, typename VT::V* __restri
       const cplx<R> d = sd[jj[it]];
 #pragma unroll
       for (int l = 0; l < VT::L; ++l) {
+        if (VT::L == 2 && p.lanectl >= 0 && l != p.lanectl) continue;
         R ar, ai, orr, oi;
         VT::get(v[it], l, ar, ai);
         cmul_numpy(d.x, d.y, ar, ai, orr, oi);
@@ -210,12 +212,13 @@ k_diag(const __grid_constant__ DiagP<typename VT::R> p, typename VT::V* __restri
 
 template <class VT>
 static cudaError_t diag_t(const Geom& g, int k, const int* tb, const void* diag,
-                          const unsigned char* active, void* sv, cudaStream_t st) {
+                          const unsigned char* active, void* sv, cudaStream_t st, int lanectl = -1) {
   using R = typename VT::R;
   constexpr int ITEMS = sizeof(typename VT::V) == 16 ? 4 : 8;
   DiagP<R> p;
   p.g = g;
   p.k = k;
+  p.lanectl = lanectl;
   for (int m = 0; m < DSV_MAX_TARGETS_; ++m) p.tb[m] = (m < k && tb) ? tb[m] : 0;
   const cplx<R>* d = static_cast<const cplx<R>*>(diag);
   for (int j = 0; j < (1 << k); ++j) {
@@ -229,6 +232,11 @@ static cudaError_t diag_t(const Geom& g, int k, const int* tb, const void* diag,
   if (blocks > cap) blocks = cap;
   k_diag<VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
   return cudaGetLastError();
+}
+
+cudaError_t launch_diag_lane(const Geom& g, const void* diag, int lanectl, void* sv, cudaStream_t st) {
+  const unsigned char one = 1;
+  return diag_t<C64x2>(g, 0, nullptr, diag, &one, sv, st, lanectl);
 }
 
 cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb, const void* diag,
