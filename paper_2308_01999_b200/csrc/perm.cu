@@ -36,7 +36,7 @@ struct PermItems {
   static constexpr int value = bytes >= 64 ? 1 : 64 / bytes;
 };
 
-template <int K, class VT, int ITEMS>
+template <int K, class VT, int ITEMS, bool LANECTL = false>
 __global__ void __launch_bounds__(256)
 k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __restrict__ sv) {
   using V = typename VT::V;
@@ -69,7 +69,7 @@ k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __res
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         R ar, ai, orr, oi;
-        if (L == 2 && p.lanectl >= 0 && l != p.lanectl) {  // control not met: the destination keeps its lane
+        if (LANECTL && l != p.lanectl) {  // control not met: the destination keeps its lane
 #pragma unroll
           for (int q = 0; q < D; ++q)
             if (q == p.pdst[j]) VT::get(in[it][q], l, orr, oi);
@@ -108,7 +108,14 @@ static cudaError_t perm_reg_t(const Geom& g, const uint64_t* offs_in, const uint
   const uint64_t per_block = 256ull * ITEMS;
   const uint64_t blocks = (g.nwork + per_block - 1) / per_block;
   if (blocks == 0 || active == 0) return cudaSuccess;
-  k_perm<K, VT, ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  if (lanectl >= 0) {
+    if constexpr (VT::L == 2)
+      k_perm<K, VT, ITEMS, true><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+    else
+      return cudaErrorInvalidValue;
+  } else {
+    k_perm<K, VT, ITEMS, false><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<typename VT::V*>(sv));
+  }
   return cudaGetLastError();
 }
 
