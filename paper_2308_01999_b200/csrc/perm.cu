@@ -26,7 +26,8 @@ struct PermP {
   uint64_t active;  // bit j set: entry j moves or scales
   uint64_t offs_in[1 << K];
   uint64_t offs_out[1 << K];  // offs[perm[j]]
-  uint8_t pdst[1 << K];       // perm[j] (lanectl: the destination's other lane keeps its own value)
+  uint32_t psel[1 << K];      // lanectl: bit perm[j] set (the destination's other lane keeps its own value;
+                              // a one-hot mask, not an index, so in[][] stays in registers)
   cplx<R> d[1 << K];
 };
 
@@ -70,9 +71,16 @@ k_perm(const __grid_constant__ PermP<K, typename VT::R> p, typename VT::V* __res
       for (int l = 0; l < L; ++l) {
         R ar, ai, orr, oi;
         if (LANECTL && l != p.lanectl) {  // control not met: the destination keeps its lane
+          orr = R(0);
+          oi = R(0);
 #pragma unroll
-          for (int q = 0; q < D; ++q)
-            if (q == p.pdst[j]) VT::get(in[it][q], l, orr, oi);
+          for (int q = 0; q < D; ++q) {
+            R tr, ti;
+            VT::get(in[it][q], l, tr, ti);
+            const bool s = (p.psel[j] >> q) & 1u;
+            orr = s ? tr : orr;
+            oi = s ? ti : oi;
+          }
         } else {
           VT::get(in[it][j], l, ar, ai);
           cmul_numpy(dr, di, ar, ai, orr, oi);
@@ -95,7 +103,7 @@ static cudaError_t perm_reg_t(const Geom& g, const uint64_t* offs_in, const uint
   p.g = g;
   p.active = active;
   p.lanectl = lanectl;
-  for (int j = 0; j < D; ++j) p.pdst[j] = pdst ? pdst[j] : uint8_t(j);
+  for (int j = 0; j < D; ++j) p.psel[j] = 1u << (pdst ? pdst[j] : j);
   uint64_t span = 0;
   for (int j = 0; j < D; ++j) span |= offs_in[j];
   p.cached = span != 0 && span * sizeof(typename VT::V) < 256;
