@@ -930,9 +930,12 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   DeviceGuard g(s->device);
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * std::ldexp(1.0, s->nbits - nctrl);
   const uint64_t D = 1ull << k;
-  // plain k = 4 stays on the CUDA cores (HBM-bound there: 6.3 TB/s vs 4.8 on
-  // the tensor path) except on the lowest four bits (CUDA cores: 2 TB/s)
-  if ((k == 5 || k == 6 || (k == 4 && tc_mode(gg) == 2)) && tc_eligible(s, gg))
+  // plain k = 4 stays on the CUDA cores (random unitaries at n = 33: 0.80-0.89
+  // of peak, the tensor path 0.77-0.88) except on the lowest four bits (CUDA
+  // cores: 2 TB/s) and with index bit 0 a target (16-byte member pairs on the
+  // tensor path: (0,5,17,30) 28.0 -> 22.6 ms)
+  const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env));
+  if ((k == 5 || k == 6 || tc4) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
   if (g_wt_env && nctrl == 0 && k >= 1 && k <= 4 && gg.tsorted[k - 1] < 6 && s->nbits >= 10) {

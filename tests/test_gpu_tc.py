@@ -121,6 +121,30 @@ def test_tc_dense_low_bits_vs_oracle(case):
     assert _rel_err(sv.amplitudes, want) <= REL
 
 
+@pytest.mark.parametrize("targets,ctrls", [([0, 5, 9, 14], []), ([0, 2, 3, 4], []),
+                                           ([0, 6, 7, 8], [(12, 1)]), ([0, 3, 10, 15], [(13, 0)])])
+def test_tc_k4_bit0_target_vs_oracle(targets, ctrls):
+    """Plain k = 4 with index bit 0 a target takes the tensor path (16-byte
+    member pairs); every other k = 4 layout except bits 0..3 stays on the CUDA cores."""
+    rng = np.random.default_rng(sum(targets))
+    n = 16
+    targets = [int(t) for t in rng.permutation(targets)]
+    st = random_state(n, rng, np.complex64)
+    m = G.random_unitary(16, rng)
+    want = st.astype(np.complex128)
+    O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), targets, ctrls)
+    sv = StateVector.from_amplitudes(st)
+    nat = _tc_launches(sv)
+    sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
+    assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1
+    assert np.abs(sv.amplitudes - want).max() <= 1e-5
+    assert _rel_err(sv.amplitudes, want) <= REL
+    sv2 = StateVector.from_amplitudes(st)
+    nat = _tc_launches(sv2)
+    sv2.apply_matrix(G.DenseGate(m, (1, 5, 9, 14)))
+    assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 0  # bit 0 free: CUDA cores
+
+
 @pytest.mark.parametrize("k", [4, 5])
 def test_tc_phased_vs_oracle(k):
     rng = np.random.default_rng(950 + k)
