@@ -65,6 +65,12 @@ const bool g_lowt_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// 64-byte-block kernel for complex64 permutations inside bits 0..2 (perm.cu); DSV_BLK8=0 disables.
+const bool g_blk8_env = [] {
+  const char* e = std::getenv("DSV_BLK8");
+  return !(e && e[0] == '0');
+}();
+
 // Warp-transpose kernel for dense gates inside the lowest 6 bits (wt.cu); DSV_WT=0 disables.
 const bool g_wt_env = [] {
   const char* e = std::getenv("DSV_WT");
@@ -1347,6 +1353,17 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
     for (uint64_t j = 0; j < D; ++j) av[j] = act[j];
     ProfTok t = prof_start(s);
     CKL(launch_diag(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, k, geo, tb, dn.data(), av.data(), s->d, s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
+  if (g_blk8_env && s->dtype == DSV_C64 && nctrl == 0 && k >= 1 && k <= 3 && gg.tsorted[k - 1] < 3 &&
+      s->nbits >= 3) {
+    // every group inside one 64-byte block: full-sector 32-byte accesses
+    uint64_t active = 0;
+    for (uint64_t j = 0; j < D; ++j)
+      if (act[j]) active |= 1ull << j;
+    ProfTok t = prof_start(s);
+    CKL(launch_perm_blk8(s->nbits, k, gg.tsorted.data(), pn.data(), dn.data(), active, s->d, s->stream), 1);
     prof_stop(s, t, PC_PERM, bytes);
     return DSV_OK;
   }

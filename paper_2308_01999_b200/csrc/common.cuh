@@ -96,6 +96,13 @@ __device__ __forceinline__ void stcs32(void* p, float a, float b, float c, float
                : "memory");
 }
 
+// 32-byte streaming load (sm_100: LDG.256)
+__device__ __forceinline__ void ldcs32(const void* p, float (&v)[8]) {
+  asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
 // y = M x for one amplitude group held in registers (L lanes = groups per
 // unit), streamed out row by row.  Complex products in the 3-multiplication
 // (Gauss) form: with a + ib = M[r][c] and x + iy = x_c,

@@ -11,6 +11,8 @@
 // set is closed under perm, so reading only active inputs and writing only
 // active outputs is complete.  For an unfused controlled phase this halves
 // the touched amplitudes on top of the control subcube (2*s*2^(n-2) bytes).
+#include <cstring>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -259,6 +261,88 @@ cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb
   if (dtype == 1) return diag_t<C128x1>(g, k, tb, diag, active, sv, st);
   if (mode == MODE_VEC2) return diag_t<C64x2>(g, k, tb, diag, active, sv, st);
   return diag_t<C64x1>(g, k, tb, diag, active, sv, st);
+}
+
+// ---- complex64 permutations inside index bits 0..2 (no controls) ------------
+// Every group lies inside one 64-byte block of 8 amplitudes, so one thread
+// owns a block: two 32-byte loads, the permutation applied in registers,
+// two 32-byte stores.  A warp instruction covers 1 KB of full sectors (the
+// register path strides its lanes 32-64 bytes apart here).  Output slot q
+// takes in[src[q]] scaled by d[q] (NumPy FMA form), or copied when its
+// table entry is inactive; the source is picked by one-hot selects so the
+// block stays in registers.
+struct Blk8P {
+  uint64_t nblk;
+  uint32_t srcsel[8];   // bit p set: out[q] comes from in[p]
+  uint32_t scaled;      // bit q set: out[q] = d[q] * in[src]
+  cplx<float> d[8];
+};
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_perm_blk8(const __grid_constant__ Blk8P p, float* __restrict__ sv) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * (256u * ITEMS) + threadIdx.x;
+  float v[ITEMS][2][8];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t b = b0 + uint64_t(it) * 256u;
+    if (b < p.nblk) {
+      ldcs32(sv + b * 16, v[it][0]);
+      ldcs32(sv + b * 16 + 8, v[it][1]);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t b = b0 + uint64_t(it) * 256u;
+    if (b >= p.nblk) continue;
+    float o[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float ar = 0.f, ai = 0.f;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const bool on = (p.srcsel[q] >> s) & 1u;
+        ar = on ? v[it][s >> 2][2 * (s & 3)] : ar;
+        ai = on ? v[it][s >> 2][2 * (s & 3) + 1] : ai;
+      }
+      if ((p.scaled >> q) & 1u) {
+        float r, i;
+        cmul_numpy(p.d[q].x, p.d[q].y, ar, ai, r, i);
+        ar = r;
+        ai = i;
+      }
+      o[2 * q] = ar;
+      o[2 * q + 1] = ai;
+    }
+    stcs32(sv + b * 16, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+    stcs32(sv + b * 16 + 8, o[8], o[9], o[10], o[11], o[12], o[13], o[14], o[15]);
+  }
+}
+
+cudaError_t launch_perm_blk8(int nbits, int k, const int* tb, const uint64_t* pout, const void* diag,
+                             uint64_t active, void* sv, cudaStream_t st) {
+  if (nbits < 3 || k < 1 || k > 3) return cudaErrorInvalidValue;
+  const cplx<float>* d = static_cast<const cplx<float>*>(diag);  // state dtype
+  Blk8P p;
+  std::memset(&p, 0, sizeof p);
+  p.nblk = 1ull << (nbits - 3);
+  for (int q = 0; q < 8; ++q) {
+    p.srcsel[q] = 1u << q;  // untouched by default
+    p.d[q] = cplx<float>{1.f, 0.f};
+  }
+  for (int pos = 0; pos < 8; ++pos) {
+    int j = 0;
+    for (int m = 0; m < k; ++m) j |= ((pos >> tb[m]) & 1) << m;
+    if (!((active >> j) & 1ull)) continue;
+    int q = pos;
+    for (int m = 0; m < k; ++m) q = (q & ~(1 << tb[m])) | int(((pout[j] >> m) & 1ull) << tb[m]);
+    p.srcsel[q] = 1u << pos;
+    p.scaled |= 1u << q;
+    p.d[q] = d[j];
+  }
+  constexpr int ITEMS = 2;
+  const uint64_t blocks = (p.nblk + 256ull * ITEMS - 1) / (256ull * ITEMS);
+  k_perm_blk8<ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<float*>(sv));
+  return cudaGetLastError();
 }
 
 // ---- generic path: k <= 10, one CTA per group through shared memory -----------

@@ -305,6 +305,25 @@ def test_genperm_low_bits_warp_transposed_bit_exact(dtype, k):
         _check(sv.amplitudes, want, dtype, exact=True)
 
 
+@pytest.mark.parametrize("targets", [(0,), (1,), (2,), (0, 1), (1, 0), (2, 0), (1, 2), (0, 1, 2), (2, 0, 1)])
+def test_genperm_inside_bits_0_2_bit_exact(targets):
+    """complex64 permutations whose targets all lie in bits 0..2 (perm.cu
+    k_perm_blk8: one 64-byte block per thread, 32-byte accesses), identity
+    entries included: bit-exact vs the oracle."""
+    rng = np.random.default_rng(sum(targets) * 7 + len(targets))
+    k = len(targets)
+    for n in (3, 4, 11, 14):
+        st = random_state(n, rng, np.complex64)
+        diag = np.exp(1j * rng.uniform(0, 2 * np.pi, 1 << k))
+        diag[rng.random(1 << k) < 0.4] = 1.0
+        perm = rng.permutation(1 << k)
+        want = st.copy()
+        O.apply_genperm(want, n, perm, diag, list(targets), [])
+        sv = sv_from(st)
+        sv.apply_generalized_permutation(G.PermutationGate(perm, diag, targets))
+        _check(sv.amplitudes, want, np.complex64, exact=True)
+
+
 @pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
 def test_swaps_many_pairs_bit_exact(dtype):
     rng = np.random.default_rng(5)

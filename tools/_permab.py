@@ -17,6 +17,6 @@ tm(G.cx(0, 32), 0.5, "cx c0 t32")
 tm(G.cx(0, 5), 0.5, "cx c0 t5")
 tm(G.cx(4, 3), 0.5, "cx c4 t3")
 tm(G.cx(18, 17), 0.5, "cx c18 t17")
-for tg in ((0, 1), (4, 5), (31, 32), (0, 1, 2), (4, 5, 6), (2, 20)):
+for tg in ((0, 1), (1, 2), (0, 2), (0,), (0, 1, 2), (4, 5, 6), (2, 20)):
     k = len(tg); perm = rng.permutation(1 << k)
     tm(G.PermutationGate(perm, np.ones(1 << k), tg), 1.0, f"perm {tg}")
