@@ -1237,6 +1237,23 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
   bool is_diag = true;
   for (uint64_t j = 0; j < D; ++j) is_diag = is_diag && pn[j] == j;
   const int kk = k + nctrl;
+  if (g_blk8_env && s->dtype == DSV_C64 && s->nbits >= 3 && k >= 1 && gg.holes.back() < 3 && gg.holes[0] <= 1 &&
+      (nctrl == 0 || is_diag || gg.holes[0] == 0)) {
+    // targets and controls inside bits 0..2, touching bit 0 or 1 (CP(0, 1),
+    // SWAP(0, 1), 2-3 qubit permutations on the lowest bits ...): every group
+    // inside one 64-byte block, one full pass with full-sector 32-byte accesses
+    // (n = 33: 22-25 -> 19.7 ms).  Kept on the other kernels: holes = {2} alone
+    // and permutations controlled above bit 0 (CX(2, 1): 16.1 ms there), whose
+    // 32-byte runs let the untouched half skip its writes.
+    uint64_t active = 0;
+    for (uint64_t j = 0; j < D; ++j)
+      if (act[j]) active |= 1ull << j;
+    ProfTok t = prof_start(s);
+    CKL(launch_perm_blk8(s->nbits, k, gg.tsorted.data(), pn.data(), dn.data(), active, cb, cv, nctrl, s->d,
+                         s->stream), 1);
+    prof_stop(s, t, PC_PERM, bytes);
+    return DSV_OK;
+  }
   if (is_diag && nactive == 1 && s->dtype == DSV_C64 && s->nbits >= 2 && !gg.holes.empty() && gg.holes[0] == 0 &&
       (gg.holes.size() < 2 || gg.holes[1] >= 2)) {  // (bit 1 fixed too: units 32 B apart, the stream kernel wins)
     // the same with index bit 0 fixed (target or control): 16-byte units over
@@ -1353,17 +1370,6 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
     for (uint64_t j = 0; j < D; ++j) av[j] = act[j];
     ProfTok t = prof_start(s);
     CKL(launch_diag(s->dtype, vec2 ? MODE_VEC2 : MODE_SCALAR, k, geo, tb, dn.data(), av.data(), s->d, s->stream), 1);
-    prof_stop(s, t, PC_PERM, bytes);
-    return DSV_OK;
-  }
-  if (g_blk8_env && s->dtype == DSV_C64 && nctrl == 0 && k >= 1 && k <= 3 && gg.tsorted[k - 1] < 3 &&
-      s->nbits >= 3) {
-    // every group inside one 64-byte block: full-sector 32-byte accesses
-    uint64_t active = 0;
-    for (uint64_t j = 0; j < D; ++j)
-      if (act[j]) active |= 1ull << j;
-    ProfTok t = prof_start(s);
-    CKL(launch_perm_blk8(s->nbits, k, gg.tsorted.data(), pn.data(), dn.data(), active, s->d, s->stream), 1);
     prof_stop(s, t, PC_PERM, bytes);
     return DSV_OK;
   }

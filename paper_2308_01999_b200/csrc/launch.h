@@ -85,10 +85,11 @@ cudaError_t launch_dense_low(int k, const LowDesc& d, const void* matrix, const 
 // generalised permutation with all targets in bits 0..5 (no controls), warp-transposed (wt.cu)
 cudaError_t launch_perm_wt(int dtype, int nbits, int k, const int* tb, const uint64_t* pout, const void* diag,
                            uint64_t active, void* sv, cudaStream_t st);
-// complex64 generalised permutation with all targets in bits 0..2 (no controls):
+// complex64 generalised permutation with all targets and controls in bits 0..2:
 // one 64-byte block per thread, 32-byte loads/stores (perm.cu)
 cudaError_t launch_perm_blk8(int nbits, int k, const int* tb, const uint64_t* pout, const void* diag,
-                             uint64_t active, void* sv, cudaStream_t st);
+                             uint64_t active, const int32_t* cb, const int32_t* cv, int nctrl, void* sv,
+                             cudaStream_t st);
 cudaError_t launch_dense_wt(int dtype, int nbits, int k, const int* tb, const void* matrix, void* sv,
                             cudaStream_t st);
 // k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem

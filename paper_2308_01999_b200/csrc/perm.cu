@@ -263,7 +263,7 @@ cudaError_t launch_diag(int dtype, int mode, int k, const Geom& g, const int* tb
   return diag_t<C64x1>(g, k, tb, diag, active, sv, st);
 }
 
-// ---- complex64 permutations inside index bits 0..2 (no controls) ------------
+// ---- complex64 permutations / diagonals inside index bits 0..2 ---------------
 // Every group lies inside one 64-byte block of 8 amplitudes, so one thread
 // owns a block: two 32-byte loads, the permutation applied in registers,
 // two 32-byte stores.  A warp instruction covers 1 KB of full sectors (the
@@ -319,8 +319,9 @@ __global__ void __launch_bounds__(256) k_perm_blk8(const __grid_constant__ Blk8P
 }
 
 cudaError_t launch_perm_blk8(int nbits, int k, const int* tb, const uint64_t* pout, const void* diag,
-                             uint64_t active, void* sv, cudaStream_t st) {
-  if (nbits < 3 || k < 1 || k > 3) return cudaErrorInvalidValue;
+                             uint64_t active, const int32_t* cb, const int32_t* cv, int nctrl, void* sv,
+                             cudaStream_t st) {
+  if (nbits < 3 || k < 1 || k + nctrl > 3) return cudaErrorInvalidValue;
   const cplx<float>* d = static_cast<const cplx<float>*>(diag);  // state dtype
   Blk8P p;
   std::memset(&p, 0, sizeof p);
@@ -333,6 +334,9 @@ cudaError_t launch_perm_blk8(int nbits, int k, const int* tb, const uint64_t* po
     int j = 0;
     for (int m = 0; m < k; ++m) j |= ((pos >> tb[m]) & 1) << m;
     if (!((active >> j) & 1ull)) continue;
+    bool ctl_met = true;  // controls (also inside bits 0..2): unmet slots stay as they are
+    for (int c = 0; c < nctrl; ++c) ctl_met = ctl_met && ((pos >> cb[c]) & 1) == cv[c];
+    if (!ctl_met) continue;
     int q = pos;
     for (int m = 0; m < k; ++m) q = (q & ~(1 << tb[m])) | int(((pout[j] >> m) & 1ull) << tb[m]);
     p.srcsel[q] = 1u << pos;

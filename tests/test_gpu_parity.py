@@ -324,6 +324,27 @@ def test_genperm_inside_bits_0_2_bit_exact(targets):
         _check(sv.amplitudes, want, np.complex64, exact=True)
 
 
+@pytest.mark.parametrize("targets,ctrls", [((0,), ((1, 1),)), ((1,), ((0, 0),)), ((0, 2), ((1, 1),)),
+                                           ((2,), ((0, 1), (1, 0))), ((1, 2), ((0, 1),))])
+@pytest.mark.parametrize("kind", ["perm", "diag", "phase1"])
+def test_controlled_genperm_inside_bits_0_2_bit_exact(targets, ctrls, kind):
+    """CX(1, 0), CP(0, 1), controlled diagonals ... with targets AND controls in
+    bits 0..2 (k_perm_blk8): bit-exact vs the oracle."""
+    rng = np.random.default_rng(len(targets) * 31 + len(ctrls) + len(kind))
+    k = len(targets)
+    for n in (3, 5, 12):
+        st = random_state(n, rng, np.complex64)
+        diag = np.exp(1j * rng.uniform(0, 2 * np.pi, 1 << k))
+        perm = rng.permutation(1 << k) if kind == "perm" else np.arange(1 << k)
+        if kind == "phase1":  # single-entry diagonal (controlled phase)
+            diag[:-1] = 1.0
+        want = st.copy()
+        O.apply_genperm(want, n, perm, diag, list(targets), list(ctrls))
+        sv = sv_from(st)
+        sv.apply_generalized_permutation(G.PermutationGate(perm, diag, targets, ctrls))
+        _check(sv.amplitudes, want, np.complex64, exact=True)
+
+
 @pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
 def test_swaps_many_pairs_bit_exact(dtype):
     rng = np.random.default_rng(5)
