@@ -65,6 +65,12 @@ const bool g_lowt_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// 64-byte-block kernel for complex64 dense gates inside bits 0..2 (perm.cu); DSV_DBLK8=0 disables.
+const bool g_dblk8_env = [] {
+  const char* e = std::getenv("DSV_DBLK8");
+  return !(e && e[0] == '0');
+}();
+
 // 64-byte-block kernel for complex64 permutations inside bits 0..2 (perm.cu); DSV_BLK8=0 disables.
 const bool g_blk8_env = [] {
   const char* e = std::getenv("DSV_BLK8");
@@ -943,6 +949,21 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env));
   if ((k == 5 || k == 6 || tc4) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
+  bool ctl_bit0 = false;
+  for (int c = 0; c < nctrl; ++c) ctl_bit0 = ctl_bit0 || cb[c] == 0;
+  if (g_dblk8_env && s->dtype == DSV_C64 && k >= 2 && s->nbits >= 3 && gg.holes.back() < 3 && gg.holes[0] <= 1 &&
+      (nctrl == 0 || ctl_bit0)) {
+    // targets and controls inside bits 0..2: the 8 x 8 block operator on one
+    // 64-byte block per thread (32-byte accesses).  n = 33: (1,2) 23.0 -> 19.6 ms,
+    // (0,2) 23.6 -> 19.6, (0,1,2) 21.6 -> 19.5, (1,2) controlled by bit 0 24.6 ->
+    // 19.5; a control on bit 2 keeps the low kernels (they skip the unmet half: 18.5)
+    std::vector<cplx<float>> m;
+    canon_matrix<float>(gg, matrix, m);
+    ProfTok t = prof_start(s);
+    CKL(launch_dense_blk8(s->nbits, k, gg.tsorted.data(), m.data(), cb, cv, nctrl, s->d, s->stream), 1);
+    prof_stop(s, t, PC_DENSE, bytes);
+    return DSV_OK;
+  }
   if (k >= 2 && low_eligible(s, gg)) return apply_low(s, gg, matrix, {}, PC_DENSE_LOW, bytes);
   if (g_wt_env && nctrl == 0 && k >= 1 && k <= 4 && gg.tsorted[k - 1] < 6 && s->nbits >= 10) {
     // the register path strides lanes >= 32 bytes apart here: transpose through smem

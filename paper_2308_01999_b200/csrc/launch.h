@@ -90,6 +90,8 @@ cudaError_t launch_perm_wt(int dtype, int nbits, int k, const int* tb, const uin
 cudaError_t launch_perm_blk8(int nbits, int k, const int* tb, const uint64_t* pout, const void* diag,
                              uint64_t active, const int32_t* cb, const int32_t* cv, int nctrl, void* sv,
                              cudaStream_t st);
+cudaError_t launch_dense_blk8(int nbits, int k, const int* tb, const void* mcanon, const int32_t* cb,
+                              const int32_t* cv, int nctrl, void* sv, cudaStream_t st);
 cudaError_t launch_dense_wt(int dtype, int nbits, int k, const int* tb, const void* matrix, void* sv,
                             cudaStream_t st);
 // k <= 5 with low targets: tiles of 2^kh rows x 2^T amplitudes through smem

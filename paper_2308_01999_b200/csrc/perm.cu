@@ -349,6 +349,87 @@ cudaError_t launch_perm_blk8(int nbits, int k, const int* tb, const uint64_t* po
   return cudaGetLastError();
 }
 
+// Dense gates with the same footprint (targets and controls inside bits
+// 0..2): the 8 x 8 block operator B (the gate on its target bits, identity
+// where a control is unmet, zero across non-target bits) is built on the
+// host; each thread applies B to its 64-byte block with fp32 FMAs.
+struct DBlk8P {
+  uint64_t nblk;
+  cplx<float> b[64];  // row-major B[q][p]
+};
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_dense_blk8(const __grid_constant__ DBlk8P p, float* __restrict__ sv) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * (256u * ITEMS) + threadIdx.x;
+  float v[ITEMS][2][8];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t b = b0 + uint64_t(it) * 256u;
+    if (b < p.nblk) {
+      ldcs32(sv + b * 16, v[it][0]);
+      ldcs32(sv + b * 16 + 8, v[it][1]);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t b = b0 + uint64_t(it) * 256u;
+    if (b >= p.nblk) continue;
+    float o[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float accr = 0.f, acci = 0.f;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const float mr = p.b[q * 8 + s].x, mi = p.b[q * 8 + s].y;
+        const float ar = v[it][s >> 2][2 * (s & 3)], ai = v[it][s >> 2][2 * (s & 3) + 1];
+        accr = fmaf(mr, ar, accr);
+        accr = fmaf(-mi, ai, accr);
+        acci = fmaf(mr, ai, acci);
+        acci = fmaf(mi, ar, acci);
+      }
+      o[2 * q] = accr;
+      o[2 * q + 1] = acci;
+    }
+    stcs32(sv + b * 16, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+    stcs32(sv + b * 16 + 8, o[8], o[9], o[10], o[11], o[12], o[13], o[14], o[15]);
+  }
+}
+
+cudaError_t launch_dense_blk8(int nbits, int k, const int* tb, const void* mcanon, const int32_t* cb,
+                              const int32_t* cv, int nctrl, void* sv, cudaStream_t st) {
+  if (nbits < 3 || k < 1 || k + nctrl > 3) return cudaErrorInvalidValue;
+  const cplx<float>* m = static_cast<const cplx<float>*>(mcanon);  // sorted-target order
+  const int D = 1 << k;
+  int tmask = 0;
+  for (int t = 0; t < k; ++t) tmask |= 1 << tb[t];
+  DBlk8P p;
+  std::memset(&p, 0, sizeof p);
+  p.nblk = 1ull << (nbits - 3);
+  for (int q = 0; q < 8; ++q)
+    for (int s = 0; s < 8; ++s) {
+      cplx<float> e{0.f, 0.f};
+      if ((q & ~tmask) == (s & ~tmask)) {
+        bool met = true;
+        for (int c = 0; c < nctrl; ++c) met = met && ((s >> cb[c]) & 1) == cv[c];
+        if (!met) {
+          if (q == s) e.x = 1.f;
+        } else {
+          int jq = 0, js = 0;
+          for (int t = 0; t < k; ++t) {
+            jq |= ((q >> tb[t]) & 1) << t;
+            js |= ((s >> tb[t]) & 1) << t;
+          }
+          e = m[jq * D + js];
+        }
+      }
+      p.b[q * 8 + s] = e;
+    }
+  constexpr int ITEMS = 2;
+  const uint64_t blocks = (p.nblk + 256ull * ITEMS - 1) / (256ull * ITEMS);
+  k_dense_blk8<ITEMS><<<dim3(unsigned(blocks)), 256, 0, st>>>(p, static_cast<float*>(sv));
+  return cudaGetLastError();
+}
+
 // ---- generic path: k <= 10, one CTA per group through shared memory -----------
 template <typename R>
 __global__ void __launch_bounds__(256)

@@ -578,3 +578,20 @@ def test_dense_controlled_by_bit0(ctl_val):
         sv = sv_from(st)
         sv.apply_matrix(G.DenseGate(m, targets, tuple(ctrls)))
         assert np.abs(sv.amplitudes - want).max() <= 1e-5 * np.abs(want).max() * 4
+
+
+@pytest.mark.parametrize("targets,ctrls", [((0, 1), ()), ((1, 2), ()), ((2, 0), ()), ((0, 1, 2), ()), ((2, 1, 0), ()),
+                                           ((1, 2), ((0, 1),)), ((0, 2), ((1, 0),)), ((0, 1), ((2, 1),))])
+def test_dense_inside_bits_0_2_vs_oracle(targets, ctrls):
+    """complex64 dense gates with targets and controls inside bits 0..2 (perm.cu
+    k_dense_blk8: the 8 x 8 block operator per 64-byte block) vs the oracle."""
+    rng = np.random.default_rng(len(targets) * 17 + len(ctrls) + targets[0])
+    k = len(targets)
+    for n in (3, 4, 9, 13):
+        st = random_state(n, rng, np.complex64)
+        m = G.random_unitary(1 << k, rng)
+        want = st.astype(np.complex128)
+        O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), list(targets), list(ctrls))
+        sv = sv_from(st)
+        sv.apply_matrix(G.DenseGate(m, targets, ctrls))
+        _check(sv.amplitudes, want, np.complex64, exact=False)
