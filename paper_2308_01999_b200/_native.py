@@ -152,6 +152,24 @@ def dtype_code(dtype) -> int:
     raise InvalidArgumentError(f"unsupported state dtype {dt}; use complex64 or complex128")
 
 
+def _square(matrix, dtype, k: int) -> np.ndarray:
+    """Gate matrix as a contiguous 2^k x 2^k array of the state dtype; the C ABI
+    reads exactly 4^k entries, so a wrong shape is rejected here (the
+    reference's NumPy matmul raises on it, statevec.py:60)."""
+    m = np.ascontiguousarray(matrix, dtype=dtype)
+    d = 1 << k
+    if m.shape != (d, d):
+        raise InvalidArgumentError(f"matrix shape {m.shape} does not match {k} targets (expected ({d}, {d}))")
+    return m
+
+
+def _table(values, dtype, k: int, what: str) -> np.ndarray:
+    a = np.ascontiguousarray(values, dtype=dtype).reshape(-1)
+    if a.size != 1 << k:
+        raise InvalidArgumentError(f"{what} has {a.size} entries; {k} targets need {1 << k}")
+    return a
+
+
 def device_count() -> int:
     n = C.c_int(0)
     rc = lib().dsv_device_count(C.byref(n))
@@ -244,16 +262,16 @@ class NativeState:
         call("dsv_copy", self._h, other._h)
 
     def apply_matrix(self, matrix, targets, controls=()) -> None:
-        m = np.ascontiguousarray(matrix, dtype=self.dtype)
         t, tp = i32(targets)
+        m = _square(matrix, self.dtype, len(t))
         cb, cbp = i32([b for b, _ in controls])
         cv, cvp = i32([v for _, v in controls])
         call("dsv_apply_matrix", self._h, ptr(m), tp, len(t), cbp, cvp, len(cb))
 
     def apply_matrix_phased(self, matrix, targets, cross=(), outside=()) -> None:
         """cross: (target index m, outside bit, theta); outside: (bit, theta)."""
-        m = np.ascontiguousarray(matrix, dtype=self.dtype)
         t, tp = i32(targets)
+        m = _square(matrix, self.dtype, len(t))
         ct, ctp = i32([c[0] for c in cross])
         cb, cbp = i32([c[1] for c in cross])
         cth = np.ascontiguousarray([float(c[2]) for c in cross], dtype=np.float64)
@@ -264,9 +282,9 @@ class NativeState:
              oth.ctypes.data_as(_dp) if oth.size else None, len(ob))
 
     def apply_genperm(self, perm, diag, targets, controls=()) -> None:
-        p, pp = i64(perm)
-        d = np.ascontiguousarray(diag, dtype=self.dtype)
         t, tp = i32(targets)
+        p, pp = i64(_table(perm, np.int64, len(t), "permutation"))
+        d = _table(diag, self.dtype, len(t), "diagonal")
         cb, cbp = i32([b for b, _ in controls])
         cv, cvp = i32([v for _, v in controls])
         call("dsv_apply_genperm", self._h, pp, ptr(d), tp, len(t), cbp, cvp, len(cb))
@@ -306,8 +324,8 @@ class NativeState:
         return complex(out[0], out[1])
 
     def expect_matrix(self, matrix, targets) -> complex:
-        m = np.ascontiguousarray(matrix, dtype=self.dtype)
         t, tp = i32(targets)
+        m = _square(matrix, self.dtype, len(t))
         out = np.zeros(2, dtype=np.float64)
         call("dsv_expect_matrix", self._h, ptr(m), tp, len(t), out.ctypes.data_as(_dp))
         return complex(out[0], out[1])

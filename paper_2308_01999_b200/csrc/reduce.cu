@@ -517,13 +517,23 @@ k_sample_scan(const V* __restrict__ sv, uint64_t namps, uint64_t chunk_amps, int
   if (end > namps) end = namps;
   const double target = resid[s];
   double run = 0.0;
-  uint64_t found = end - 1;  // rounding fallback: last amplitude of the chunk
+  // rounding fallback (the in-chunk scan sums in a different order than the
+  // chunk totals): the last amplitude of the chunk with nonzero probability,
+  // so a shot never lands on an impossible outcome (the reference clips to a
+  // valid index, statevec.py:270-272)
+  uint64_t found = end - 1;
+  bool any_nz = false;
   for (uint64_t i0 = begin; i0 < end; i0 += 32) {
     const uint64_t i = i0 + lane;
     double p = 0.0;
     if (i < end) {
       const V a = sv[i];
       p = double(a.x) * double(a.x) + double(a.y) * double(a.y);
+    }
+    const unsigned nz = __ballot_sync(0xffffffffu, p > 0.0);
+    if (nz) {
+      found = i0 + 31 - __clz(nz);
+      any_nz = true;
     }
     // inclusive scan across the warp
 #pragma unroll
@@ -534,11 +544,12 @@ k_sample_scan(const V* __restrict__ sv, uint64_t namps, uint64_t chunk_amps, int
     const unsigned hit = __ballot_sync(0xffffffffu, (i < end) && (run + p > target));
     if (hit) {
       found = i0 + __ffs(hit) - 1;
+      any_nz = true;
       break;
     }
     run += __shfl_sync(0xffffffffu, p, 31);
   }
-  if (lane == 0) out[s] = found;
+  if (lane == 0) out[s] = any_nz ? found : end - 1;
 }
 
 cudaError_t launch_sample_scan(int dtype, uint64_t namps, uint64_t chunk_amps, int64_t shots,

@@ -35,6 +35,7 @@ from .plan import (
     split_controls,
     swap_transfer,
 )
+from .mirror import mirror_of
 from .statevec import StateVector
 
 __all__ = ["Exchange", "ReorderPlan", "TransferStats", "SegmentedStateVector"]
@@ -115,8 +116,13 @@ class SegmentedStateVector:
             for st, m in zip(self._devs, self._mirrors):
                 st.download(m)
             self._mirror_valid = True
-        self._host_dirty = True
-        return self._mirrors
+        # writes into a segment array flag the mirrors for upload (mirror.py);
+        # reads alone never re-upload
+        return _Mirrors(mirror_of(m, self.mark_host_dirty) for m in self._mirrors)
+
+    def mark_host_dirty(self) -> None:
+        if self._mirrors is not None and self._mirror_valid:
+            self._host_dirty = True
 
     def _sync_in(self) -> None:
         if self._host_dirty and self._mirror_valid and self._mirrors is not None:

@@ -183,6 +183,7 @@ class DistributedStateVector:
             self.seg = segment_factory(self.comm, self.local_bits, self.dtype)
         self.qubit_map = list(range(num_qubits))
         self.stats = TransferStats()
+        self._basis0 = True  # a fresh segment set is |0...0>
 
     # -- layout --------------------------------------------------------------------------
     def reset(self) -> None:

@@ -7,7 +7,8 @@ through the C ABI.  ``amplitudes`` is a host mirror kept coherent lazily:
 
 * reading it downloads the device state once and hands out the mirror;
 * the caller may write into the mirror in place (the reference's tests do
-  ``sv.amplitudes[:] = ...``) — the next device operation re-uploads it;
+  ``sv.amplitudes[:] = ...``) — the write is noticed (mirror.MirrorArray)
+  and the next device operation re-uploads it; plain reads never do;
 * any device operation invalidates the mirror.
 
 Logical qubits resolve to physical index bits through ``bit_map``, which
@@ -26,6 +27,7 @@ import numpy as np
 from . import _native as N
 from .core import InvalidArgumentError, check_swap_pairs
 from .gates import DenseGate, Gate, PauliString, PermutationGate
+from .mirror import mirror_of
 
 _DEGENERATE_NORM = 1e-12  # statevec.py:19
 
@@ -87,8 +89,15 @@ class StateVector:
                 self._mirror = np.empty(1 << self.num_qubits, dtype=self.dtype)
             self._dev.download(self._mirror)
             self._mirror_valid = True
-        self._host_dirty = True  # handed out: the caller may write into it
-        return self._mirror
+        # writes into the handed-out array (in place, through views, np.copyto
+        # ...) flag it for upload before the next device operation; reads do not
+        return mirror_of(self._mirror, self.mark_host_dirty)
+
+    def mark_host_dirty(self) -> None:
+        """The mirror returned by ``amplitudes`` was modified (needed only
+        after writes through raw buffers, which MirrorArray cannot see)."""
+        if self._mirror is not None and self._mirror_valid:
+            self._host_dirty = True
 
     @amplitudes.setter
     def amplitudes(self, values) -> None:
