@@ -8,9 +8,17 @@ Workload (BASELINE.json configs[2], the config its metric is quoted on):
 k = 5 with the phase-folding fuser (fusion_fold.py: 7 dense/phased windows,
 SWAPs as relabels; the reference's FusionConfig(5, 6) gives 152 ops and is
 timed beside it), run from |0...0> on one B200.  A "step" = reset to |0> +
-the whole fused circuit.  At N > 1 (torchrun, one process per GPU) the same 33-qubit
-circuit is sharded over N GPUs by its top log2 N qubits (strong scaling, as
-in the paper's PAPER.md:285-298 table) with P2P global<->local swaps.
+the whole fused circuit.  At N > 1 the same 33-qubit circuit is sharded over
+N GPUs by its top log2 N qubits (strong scaling, as in the paper's
+PAPER.md:285-298 table) with batched P2P global<->local exchanges; ONE host
+process drives all N GPUs (shard.py, torch-free), so a plain
+`python bench.py --gpus N` works (under torchrun rank 0 does it and the other
+ranks exit; DSV_BENCH_MULTIPROC=1 selects the one-process-per-GPU layer of
+multigpu.py instead).  The N > 1 line also carries BASELINE configs 4 and 5
+as `legs`: QV-34 complex128 on 2 / 4 GPUs, random-36 complex64 on 4 / 8 GPUs
+with expectation values, and at N = 8 the weak-scaling efficiency
+T(random-33, 1 GPU) / T(random-36, 8 GPUs).  On a box with fewer GPUs than N
+the segments share the devices ("virtual_devices") and the legs are skipped.
 
 value   = circuit gates (577) / device time per step (CUDA events on the
           state's stream, max over ranks), inputs resident in HBM;
@@ -369,6 +377,170 @@ def run_single(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ---- N > 1: one host process drives N GPUs (shard.py, torch-free) -------------------------------
+
+def _sharded_time(sv, ops, steps: int, warmup: int, reset=True):
+    """Device time per step of `ops` on a ShardedStateVector: CUDA events on
+    every segment's stream, max over segments (the exchanges join the
+    streams, so each span covers the work it waited for)."""
+    def step():
+        if reset:
+            sv.reset()
+        sv.run(ops)
+
+    for _ in range(warmup):
+        step()
+    sv.sync()
+    sv.event_record(0)
+    for _ in range(steps):
+        step()
+    sv.event_record(1)
+    sv.sync()
+    return sv.event_elapsed_max(0, 1) / steps
+
+
+def _exchange_gbs(profs) -> dict:
+    """NVLink-side rate of the masked exchanges: 2 x 16 bytes cross the link
+    per exchanged unit (one read + one write of the partner's half)."""
+    ms = sum(p.get("exchange", {}).get("ms", 0.0) for p in profs)
+    by = sum(p.get("exchange", {}).get("bytes", 0.0) for p in profs)
+    if not ms:
+        return {"launches": 0}
+    return {"launches": int(sum(p.get("exchange", {}).get("count", 0) for p in profs)),
+            "ms_sum_over_devices": ms, "hbm_GB_per_s_per_device": by / (ms / 1000.0) / 1e9,
+            "link_GB_per_s_per_device_per_direction": by / 4.0 / (ms / 1000.0) / 1e9}
+
+
+def run_sharded(args) -> None:
+    from paper_2308_01999_b200 import _native as N
+    from paper_2308_01999_b200.circuits import gen_qv, random_gate_sequence, to_gates
+    from paper_2308_01999_b200.gates import PauliString
+    from paper_2308_01999_b200.shard import ShardedStateVector
+
+    ndev = N.device_count()
+    if ndev < 1:
+        raise RuntimeError("bench.py needs a CUDA device")
+    P = args.gpus
+    virtual = ndev < P
+    devices = [d % ndev for d in range(P)]
+    gates, ops, fuse_s = workload(args.fusion)
+    sv = ShardedStateVector(N_QUBITS, devices, np.complex64)
+    clocks = ClockSampler(devices[0]).start()
+    time.sleep(0.3)
+    sv.prof(True)
+    launches0 = N.launch_count()
+    ms_step = _sharded_time(sv, ops, args.steps, args.warmup)
+    launches = N.launch_count() - launches0
+    clk = clocks.stop()
+    profs = sv.prof_read()
+    sv.prof(False)
+    value = len(gates) / (ms_step / 1000.0)
+    p = sv.probabilities([0, 1, 2, 3])
+    check = {"norm": sv.norm_squared(), "marginal_max_dev_from_1/16": float(np.abs(p - 1 / 16).max())}
+    stats = dict(sv.stats.as_dict())
+    # dominant gate kernel class summed over devices
+    agg: dict[str, dict] = {}
+    for pr in profs:
+        for k, v in pr.items():
+            a = agg.setdefault(k, {"count": 0, "ms": 0.0, "bytes": 0.0})
+            for f in a:
+                a[f] += v[f]
+    pk = peaks()
+    dom_name, dom_v = max(((k, v) for k, v in agg.items() if k != "exchange"), key=lambda kv: kv[1]["ms"])
+    achieved = (dom_v["bytes"] / dom_v["count"]) / (dom_v["ms"] / dom_v["count"] / 1000.0) / 1e9
+    sv.close()
+    del sv
+
+    # e2e through the public API: fuse on the host, build, run, read back
+    e2e = []
+    for i in range(3):
+        t0 = time.perf_counter()
+        ops2 = fuse_ops(gates, args.fusion)
+        sv2 = ShardedStateVector(N_QUBITS, devices, np.complex64)
+        sv2.run(ops2)
+        pr2 = sv2.probabilities([0, 1, 2, 3])
+        sv2.close()
+        dt = time.perf_counter() - t0
+        if i:
+            e2e.append(dt)
+    e2e_s = statistics.median(e2e)
+
+    legs = {}
+    # DSV_BENCH_LEG_SHIFT=s runs the legs s qubits smaller (functional runs on
+    # a 1-GPU box, where the segments share one device)
+    shift = int(os.environ.get("DSV_BENCH_LEG_SHIFT", "0"))
+    if (not virtual or shift > 0) and not args.skip_legs:
+        if P in (2, 4):
+            # BASELINE config 4: QV-34 depth 30, complex128 (256 GiB), fold fuser k = 4
+            from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+            qv = to_gates(gen_qv(34 - shift, 30, seed=0))
+            qv_ops = fuse_fold(qv, 4).ops
+            s4 = ShardedStateVector(34 - shift, devices, np.complex128)
+            s4.prof(True)
+            ms = _sharded_time(s4, qv_ops, 1, 1)
+            pf = s4.prof_read()
+            legs["qv34_c128"] = {"n_qubits": 34 - shift, "gates_per_s": len(qv) / (ms / 1000.0), "ms_per_circuit": ms,
+                                 "circuit_gates": len(qv), "fused_ops": len(qv_ops),
+                                 "transfer_stats": s4.stats.as_dict(), "norm": s4.norm_squared(),
+                                 "exchange": _exchange_gbs(pf)}
+            s4.close()
+            del s4
+        if P in (4, 8):
+            # BASELINE config 5: random-36 c64 (512 GiB) + expectation values;
+            # weak-scaling efficiency against the same generator at 33 qubits on 1 GPU
+            n5 = 36 - shift
+            rnd36 = random_gate_sequence(n5, 200, np.random.default_rng(0), max_arity=2)
+            s5 = ShardedStateVector(n5, devices, np.complex64)
+            s5.prof(True)
+            ms36 = _sharded_time(s5, rnd36, 1, 1)
+            pf = s5.prof_read()
+            t0 = time.perf_counter()
+            ev = s5.expectation([PauliString(((0, "Z"), (17, "X"), (n5 - 1, "Y")))])
+            zsum = s5.expectation([PauliString(((q, "Z"),)) for q in range(n5)])
+            ev_s = time.perf_counter() - t0
+            leg = {"n_qubits": n5, "gates_per_s": len(rnd36) / (ms36 / 1000.0), "ms_per_circuit": ms36,
+                   "circuit_gates": len(rnd36), "transfer_stats": s5.stats.as_dict(),
+                   "expect_Z0X17Y35": [ev.real, ev.imag], "sum_Zq": zsum.real, "expectation_s": ev_s,
+                   "norm": s5.norm_squared(), "exchange": _exchange_gbs(pf)}
+            s5.close()
+            del s5
+            if P == 8:
+                rnd33 = random_gate_sequence(n5 - 3, 200, np.random.default_rng(0), max_arity=2)
+                s1 = ShardedStateVector(n5 - 3, [devices[0]], np.complex64)
+                ms33 = _sharded_time(s1, rnd33, 1, 1)
+                s1.close()
+                del s1
+                leg["weak_scaling"] = {"T33_1gpu_ms": ms33, "T36_8gpu_ms": ms36, "efficiency": ms33 / ms36}
+            legs["random36_c64"] = leg
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": P, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c64",
+        "data": "synthetic (QFT-33 circuit generated on the host, state starts at |0>)",
+        "config": {"workload": "qft33_c64_fused_k5", "n_qubits": N_QUBITS, "circuit_gates": len(gates),
+                   "fused_ops": len(ops), "fuse_host_s": fuse_s, "fusion": args.fusion,
+                   "global_bits": int(math.log2(P)), "devices": devices, "virtual_devices": virtual,
+                   "l2": "segments >= 8 GiB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"sv-shard{P}: one host process drives {P} GPUs (shard.py, torch-free); "
+                                  "top log2 P qubits global, batched P2P masked exchanges over NVLink"},
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"],
+                     "traffic": traffic_from_profiles(dom_name)},
+        "exchange": _exchange_gbs(profs),
+        "transfer_stats": stats,
+        "check": check,
+        "e2e": {"value": len(gates) / e2e_s, "unit": "gates/s", "seconds_per_step": e2e_s,
+                "h2d_bytes_per_step": gate_payload_bytes(ops, 8), "d2h_bytes_per_step": int(pr2.nbytes),
+                "path": "fuse + ShardedStateVector build + run + probabilities([0..3]), host wall clock"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "legs": legs,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,6 +549,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--fusion", default="fold", choices=["fold", "reference"])
+    ap.add_argument("--skip-legs", action="store_true", help="N > 1: skip the config 4 / 5 legs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -384,11 +557,19 @@ def main():
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 and os.environ.get("DSV_BENCH_MULTIPROC") == "1":
+        # one process per GPU (torch.distributed plumbing, CUDA IPC exchanges)
         from paper_2308_01999_b200 import multigpu
 
         multigpu.bench_main(args, METRIC, N_QUBITS, FUSION, PUBLISHED_1GPU_GATES_PER_S, workload, ClockSampler,
                             peaks, cpu_cores)
+        return
+    if world > 1 and int(os.environ.get("RANK", "0")) != 0:
+        # launched under torchrun: rank 0 drives every GPU from one host
+        # process (shard.py); the other ranks have nothing to do
+        return
+    if args.gpus > 1:
+        run_sharded(args)
         return
     run_single(args)
 

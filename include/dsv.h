@@ -158,6 +158,35 @@ int dsv_exchange_halves(dsv_state* a, dsv_state* b, int local_bit, int part, int
 /* whole-segment swap a <-> b (global-global pairs when both differ) */
 int dsv_exchange_all(dsv_state* a, dsv_state* b);
 
+/* Batched (global, local) index-bit swaps between two segments
+ * (distsim.py:153-198 with q global bits at once): for every offset `off`
+ * whose q local bits `lbits` are clear,
+ *     a[off | pat_a]  <->  b[off | pat_b]
+ * where pat_a / pat_b are patterns over `lbits` (pat_a = the partner's
+ * global-bit values moved onto the local bits, pat_b = a's).  q = 1,
+ * pat_a = 1 << l, pat_b = 0 is dsv_exchange_halves.  complex64 moves whole
+ * 16-byte units even when amplitude bit 0 is one of the local bits.
+ * dsv_exchange_masked runs slice `part` of `nparts` on a's device (one
+ * process per GPU: each partner runs one slice over a peer mapping). */
+int dsv_exchange_masked(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b,
+                        int part, int nparts);
+/* One process driving both devices: half of the work on a's device and
+ * stream, half on b's, both streams joined before and after (stream-ordered,
+ * no host synchronisation; peer access enabled on first use). */
+int dsv_exchange_pair(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b);
+/* make `waiter`'s stream wait for everything queued so far on `other`'s */
+int dsv_stream_join(dsv_state* waiter, dsv_state* other);
+
+/* ---- sharded reductions (one segment per device, all devices at once) ---- */
+/* The reduction of each segment is queued on its own stream, then all are
+ * collected: out[i * per + j] = value j of segment i (per = 1 for norm2,
+ * 2^k for marginals, 2 (re, im) for Pauli strings).  The caller combines the
+ * per-segment values in a fixed order (deterministic; the reference's
+ * SegmentedStateVector has no reductions of its own, BASELINE config 5). */
+int dsv_group_norm2(dsv_state** s, int count, double* out);
+int dsv_group_marginal_probs(dsv_state** s, int count, const int32_t* bits, int k, double* out);
+int dsv_group_expect_pauli(dsv_state** s, int count, const int32_t* bits, const char* paulis, int m, double* out);
+
 /* multi-process peers over NVLink: CUDA IPC handle of a segment (64 bytes) */
 int dsv_ipc_handle(dsv_state* s, void* out64);
 /* map a peer segment of the same nbits/dtype into this process as a state

@@ -70,6 +70,12 @@ SIGNATURES: dict[str, list] = {
     "dsv_sample": [_vp, _dp, C.c_int64, _u64p],
     "dsv_exchange_halves": [_vp, _vp, _int, _int, _int],
     "dsv_exchange_all": [_vp, _vp],
+    "dsv_exchange_masked": [_vp, _vp, _i32p, _int, _u64, _u64, _int, _int],
+    "dsv_exchange_pair": [_vp, _vp, _i32p, _int, _u64, _u64],
+    "dsv_stream_join": [_vp, _vp],
+    "dsv_group_norm2": [C.POINTER(_vp), _int, _dp],
+    "dsv_group_marginal_probs": [C.POINTER(_vp), _int, _i32p, _int, _dp],
+    "dsv_group_expect_pauli": [C.POINTER(_vp), _int, _i32p, C.c_char_p, _int, _dp],
     "dsv_ipc_handle": [_vp, _vp],
     "dsv_peer_open": [_int, _int, _int, _vp, C.POINTER(_vp)],
     "dsv_prof_enable": [_vp, _int],
@@ -365,6 +371,21 @@ class NativeState:
     def exchange_all(self, other: "NativeState") -> None:
         call("dsv_exchange_all", self._h, other._h)
 
+    def exchange_masked(self, other: "NativeState", lbits, pat_a: int, pat_b: int, part: int = 0,
+                        nparts: int = 1) -> None:
+        """Slice `part` of the batched exchange self[off|pat_a] <-> other[off|pat_b]."""
+        b, bp = i32(lbits)
+        call("dsv_exchange_masked", self._h, other._h, bp, len(b), int(pat_a), int(pat_b), int(part), int(nparts))
+
+    def exchange_pair(self, other: "NativeState", lbits, pat_a: int, pat_b: int) -> None:
+        """The whole batched exchange, split between both segments' devices."""
+        b, bp = i32(lbits)
+        call("dsv_exchange_pair", self._h, other._h, bp, len(b), int(pat_a), int(pat_b))
+
+    def join(self, other: "NativeState") -> None:
+        """Make this segment's stream wait for the work queued on other's."""
+        call("dsv_stream_join", self._h, other._h)
+
     def ipc_handle(self) -> bytes:
         buf = C.create_string_buffer(64)
         call("dsv_ipc_handle", self._h, buf)
@@ -397,3 +418,34 @@ class NativeState:
         out = C.c_float(0.0)
         call("dsv_event_elapsed", self._h, int(a), int(b), C.byref(out))
         return float(out.value)
+
+
+# ---- segment groups (one host thread drives every device) ---------------------------
+
+
+def _handles(states) -> C.Array:
+    arr = (_vp * len(states))(*[st._h for st in states])
+    return arr
+
+
+def group_norm2(states) -> np.ndarray:
+    """Per-segment |a|^2 sums, all devices reducing at once."""
+    out = np.zeros(len(states), dtype=np.float64)
+    call("dsv_group_norm2", _handles(states), len(states), out.ctypes.data_as(_dp))
+    return out
+
+
+def group_marginal(states, bits) -> np.ndarray:
+    b, bp = i32(bits)
+    out = np.zeros((len(states), 1 << len(b)), dtype=np.float64)
+    call("dsv_group_marginal_probs", _handles(states), len(states), bp, len(b), out.ctypes.data_as(_dp))
+    return out
+
+
+def group_expect_pauli(states, factors) -> np.ndarray:
+    """Per-segment <P> partial sums as complex values."""
+    bits, bp = i32([b for b, _ in factors])
+    ps = "".join(p for _, p in factors).encode()
+    out = np.zeros((len(states), 2), dtype=np.float64)
+    call("dsv_group_expect_pauli", _handles(states), len(states), bp, ps, len(bits), out.ctypes.data_as(_dp))
+    return out[:, 0] + 1j * out[:, 1]

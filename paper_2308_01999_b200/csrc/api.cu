@@ -160,6 +160,12 @@ struct dsv_state {
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t uev[16] = {};
+  // deferred reductions (dsv_group_*): results land in pinned host memory and
+  // the call returns before the GPU finishes
+  bool defer = false;
+  double* pinned = nullptr;
+  size_t pinned_n = 0;
+  size_t pending_n = 0;
 };
 
 namespace {
@@ -641,6 +647,23 @@ int enable_peer(int from, int to) {
 int finish_reduce(dsv_state* s, uint64_t nbins, uint64_t nchunks, int ncomp, double* d_partial,
                   double* d_out, double* host_out) {
   CKL(launch_final_sum(nbins, nchunks, ncomp, d_partial, d_out, s->stream), 1);
+  if (s->defer) {  // dsv_group_*: copy into pinned memory, collect later
+    const size_t n = size_t(nbins) * ncomp;
+    if (s->pinned_n < n) {
+      if (s->pinned) {
+        CK(cudaStreamSynchronize(s->stream));
+        CK(cudaFreeHost(s->pinned));
+        s->pinned = nullptr;
+        s->pinned_n = 0;
+      }
+      const size_t want = std::max<size_t>(n, 512);
+      CK(cudaMallocHost(&s->pinned, sizeof(double) * want));
+      s->pinned_n = want;
+    }
+    CK(cudaMemcpyAsync(s->pinned, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    s->pending_n = n;
+    return DSV_OK;
+  }
   CK(cudaMemcpyAsync(host_out, d_out, sizeof(double) * nbins * ncomp, cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
   return DSV_OK;
@@ -835,6 +858,7 @@ int dsv_state_destroy(dsv_state* s) {
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   for (auto e : s->uev)
     if (e) cudaEventDestroy(e);
+  if (s->pinned) cudaFreeHost(s->pinned);
   if (s->d && s->owned && !s->ipc && !s->exported && g_pool_env) {
     pool_put({s->device, amp_bytes(s->dtype) << s->nbits, s->d, s->stream, s->scratch, s->scratch_bytes, s->gdata,
               s->gdata_bytes});
@@ -1966,6 +1990,173 @@ int dsv_exchange_all(dsv_state* a, dsv_state* b) {
   if (!b->ipc)
     if (int rc = sync_streams(b, a)) return rc;
   return DSV_OK;
+}
+
+// ---- masked exchange (batched (global, local) swaps) ----------------------------------
+
+namespace {
+
+struct MaskedPlan {
+  Geom g;
+  int mode = MODE_SCALAR;
+  uint64_t pa = 0, pb = 0;
+  int la = 0, lb = 0;
+};
+
+int plan_masked(const dsv_state* a, const dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a,
+                uint64_t pat_b, MaskedPlan* mp) {
+  if (int rc = check_state(a)) return rc;
+  if (int rc = check_state(b)) return rc;
+  if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "exchange between segments of different shape");
+  if (q < 1 || q > 8 || !lbits) return fail(DSV_EINVAL, "masked exchange over %d bits", q);
+  uint64_t mask = 0;
+  for (int i = 0; i < q; ++i) {
+    const int l = lbits[i];
+    if (l < 0 || l >= a->nbits) return fail(DSV_EINVAL, "local bit %d out of range", l);
+    if (mask >> l & 1) return fail(DSV_EINVAL, "local bits must be distinct");
+    mask |= 1ull << l;
+  }
+  if ((pat_a | pat_b) & ~mask) return fail(DSV_EINVAL, "exchange patterns outside the local bits");
+  std::vector<int> holes;
+  if (a->dtype == DSV_C128) {
+    mp->mode = MODE_SCALAR;
+    for (int b2 = 0; b2 < 64; ++b2)
+      if (mask >> b2 & 1) holes.push_back(b2);
+    mp->pa = pat_a;
+    mp->pb = pat_b;
+    return make_geom(a->nbits, holes, 0, &mp->g);
+  }
+  // complex64: 16-byte units of amplitude pairs; bit 0 among the local bits -> lane mode
+  mp->mode = (mask & 1) ? MODE_SCALAR : MODE_VEC2;
+  mp->la = int(pat_a & 1);
+  mp->lb = int(pat_b & 1);
+  for (int b2 = 1; b2 < 64; ++b2)
+    if (mask >> b2 & 1) holes.push_back(b2 - 1);
+  mp->pa = pat_a >> 1;
+  mp->pb = pat_b >> 1;
+  return make_geom(a->nbits - 1, holes, 0, &mp->g);
+}
+
+// slice [part/nparts] of the masked exchange, launched on `run`'s stream / device
+int run_masked(dsv_state* run, dsv_state* a, dsv_state* b, const MaskedPlan& mp, int part, int nparts) {
+  const uint64_t T = mp.g.nwork;
+  const uint64_t lo = T / nparts * part + std::min<uint64_t>(part, T % nparts);
+  const uint64_t hi = lo + T / nparts + (uint64_t(part) < T % nparts ? 1 : 0);
+  ProfTok t = prof_start(run);
+  CKL(launch_exchange_masked(a->dtype, mp.mode, mp.g, mp.pa, mp.pb, mp.la, mp.lb, lo, hi, a->d, b->d, run->stream), 1);
+  // bytes: every 16-byte unit of the slice read and written on both sides
+  prof_stop(run, t, PC_EXCHANGE, 4.0 * 16.0 * double(hi - lo));
+  return DSV_OK;
+}
+
+}  // namespace
+
+int dsv_exchange_masked(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b,
+                        int part, int nparts) {
+  MaskedPlan mp;
+  if (int rc = plan_masked(a, b, lbits, q, pat_a, pat_b, &mp)) return rc;
+  if (nparts < 1 || part < 0 || part >= nparts) return fail(DSV_EINVAL, "bad exchange slice %d/%d", part, nparts);
+  DeviceGuard g(a->device);
+  if (!b->ipc && a->device != b->device)
+    if (int rc = enable_peer(a->device, b->device)) return rc;
+  if (!b->ipc)
+    if (int rc = sync_streams(a, b)) return rc;
+  if (int rc = run_masked(a, a, b, mp, part, nparts)) return rc;
+  if (!b->ipc)
+    if (int rc = sync_streams(b, a)) return rc;
+  return DSV_OK;
+}
+
+int dsv_exchange_pair(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b) {
+  MaskedPlan mp;
+  if (int rc = plan_masked(a, b, lbits, q, pat_a, pat_b, &mp)) return rc;
+  if (a->ipc || b->ipc) return fail(DSV_EINVAL, "dsv_exchange_pair needs two local segments (use dsv_exchange_masked)");
+  if (a->device != b->device) {
+    if (int rc = enable_peer(a->device, b->device)) return rc;
+    if (int rc = enable_peer(b->device, a->device)) return rc;
+  }
+  {
+    DeviceGuard g(a->device);
+    if (int rc = sync_streams(a, b)) return rc;
+  }
+  {
+    DeviceGuard g(b->device);
+    if (int rc = sync_streams(b, a)) return rc;
+  }
+  {
+    DeviceGuard g(a->device);
+    if (int rc = run_masked(a, a, b, mp, 0, 2)) return rc;
+  }
+  {
+    DeviceGuard g(b->device);
+    if (int rc = run_masked(b, a, b, mp, 1, 2)) return rc;
+  }
+  {
+    DeviceGuard g(a->device);
+    if (int rc = sync_streams(a, b)) return rc;
+  }
+  {
+    DeviceGuard g(b->device);
+    if (int rc = sync_streams(b, a)) return rc;
+  }
+  return DSV_OK;
+}
+
+int dsv_stream_join(dsv_state* waiter, dsv_state* other) {
+  if (int rc = check_state(waiter)) return rc;
+  if (int rc = check_state(other)) return rc;
+  if (waiter->ipc || other->ipc) return fail(DSV_EINVAL, "stream join of a peer mapping");
+  DeviceGuard g(waiter->device);
+  return sync_streams(waiter, other);
+}
+
+// ---- group reductions: one launch per segment, all devices concurrently ---------------------
+
+extern "C++" {
+namespace {
+
+template <class F>
+int group_reduce(dsv_state** s, int count, size_t per, double* out, F&& op) {
+  if (!s || count < 1 || !out) return fail(DSV_EINVAL, "empty segment group");
+  for (int i = 0; i < count; ++i)
+    if (int rc = check_state(s[i])) return rc;
+  int rc = DSV_OK;
+  int issued = 0;
+  for (; issued < count; ++issued) {
+    dsv_state* st = s[issued];
+    st->defer = true;
+    st->pending_n = 0;
+    rc = op(st);
+    st->defer = false;
+    if (rc) break;
+  }
+  for (int i = 0; i < issued; ++i) {
+    DeviceGuard g(s[i]->device);
+    cudaError_t e = cudaStreamSynchronize(s[i]->stream);
+    if (e != cudaSuccess && !rc) rc = cuda_fail(e, "cudaStreamSynchronize");
+    if (!rc) {
+      if (s[i]->pending_n != per) rc = fail(DSV_EINVAL, "reduction produced %zu values, expected %zu", s[i]->pending_n, per);
+      else std::memcpy(out + per * size_t(i), s[i]->pinned, sizeof(double) * per);
+    }
+  }
+  return rc;
+}
+
+}  // namespace
+}  // extern "C++"
+
+int dsv_group_norm2(dsv_state** s, int count, double* out) {
+  return group_reduce(s, count, 1, out, [](dsv_state* st) { return dsv_norm2(st, nullptr); });
+}
+
+int dsv_group_marginal_probs(dsv_state** s, int count, const int32_t* bits, int k, double* out) {
+  if (k < 0 || k > 26) return fail(DSV_EUNSUPPORTED, "marginal over %d bits not supported (max 26)", k);
+  return group_reduce(s, count, size_t(1) << k, out,
+                      [&](dsv_state* st) { return dsv_marginal_probs(st, bits, k, nullptr); });
+}
+
+int dsv_group_expect_pauli(dsv_state** s, int count, const int32_t* bits, const char* paulis, int m, double* out) {
+  return group_reduce(s, count, 2, out, [&](dsv_state* st) { return dsv_expect_pauli(st, bits, paulis, m, nullptr); });
 }
 
 int dsv_ipc_handle(dsv_state* s, void* out64) {

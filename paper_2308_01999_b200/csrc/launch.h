@@ -159,6 +159,11 @@ cudaError_t launch_scatter(int dtype, int nbits, const int32_t* ordering, uint64
 // a[off | 1<<l] <-> b[off] for off in the [lo,hi) slice of offsets with bit l clear
 cudaError_t launch_exchange_halves(int dtype, int mode, int l_unit, uint64_t lo, uint64_t hi,
                                    void* a, void* b, cudaStream_t st);
+// q-bit masked exchange a[off | pa] <-> b[off | pb] over the work items [lo, hi) of g
+// (mode MODE_VEC2: complex64 float4 units with bit 0 free; MODE_SCALAR for complex64:
+// float4 units, lanes la / lb trade places; complex128: double2 units)
+cudaError_t launch_exchange_masked(int dtype, int mode, const Geom& g, uint64_t pa, uint64_t pb, int la, int lb,
+                                   uint64_t lo, uint64_t hi, void* a, void* b, cudaStream_t st);
 cudaError_t launch_exchange_all(int dtype, uint64_t namps, void* a, void* b, cudaStream_t st);
 
 // ---- elementwise ----------------------------------------------------------

@@ -256,6 +256,55 @@ cudaError_t launch_exchange_halves(int dtype, int mode, int l_unit, uint64_t lo,
   return cudaGetLastError();
 }
 
+// Masked exchange (a batch of q (global, local) index-bit swaps between two
+// segments, distsim.py:153-198): for every offset `off` whose q local bits are
+// clear, a[off | pa] <-> b[off | pb].  Work item t enumerates those offsets in
+// unit space (g: holes at the local bits), so consecutive threads touch
+// consecutive 16-byte units whenever the low bits are free.  LANE mode
+// (complex64 with amplitude bit 0 among the local bits): units are the 16-byte
+// pairs (x, x|1); only lane `la` of a's unit and lane `lb` of b's unit trade
+// places, both units are read and written whole (no 8-byte remote accesses).
+template <typename V, bool LANE>
+__global__ void __launch_bounds__(256)
+k_exchange_masked(V* __restrict__ a, V* __restrict__ b, const __grid_constant__ Geom g, uint64_t pa, uint64_t pb,
+                  int la, int lb, uint64_t lo, uint64_t hi) {
+  for (uint64_t t = lo + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < hi;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t off = expand(g, t);
+    V* qa = a + (off | pa);
+    V* qb = b + (off | pb);
+    V x = ldg_s(qa);
+    V y = ldg_s(qb);
+    if constexpr (LANE) {
+      float2 xa = la ? make_float2(x.z, x.w) : make_float2(x.x, x.y);
+      float2 yb = lb ? make_float2(y.z, y.w) : make_float2(y.x, y.y);
+      if (la) { x.z = yb.x; x.w = yb.y; } else { x.x = yb.x; x.y = yb.y; }
+      if (lb) { y.z = xa.x; y.w = xa.y; } else { y.x = xa.x; y.y = xa.y; }
+      stg_s(qa, x);
+      stg_s(qb, y);
+    } else {
+      stg_s(qa, y);
+      stg_s(qb, x);
+    }
+  }
+}
+
+cudaError_t launch_exchange_masked(int dtype, int mode, const Geom& g, uint64_t pa, uint64_t pb, int la, int lb,
+                                   uint64_t lo, uint64_t hi, void* a, void* b, cudaStream_t st) {
+  if (hi <= lo) return cudaSuccess;
+  const unsigned gr = grid_for(hi - lo, 4);
+  if (dtype == 1)
+    k_exchange_masked<double2, false><<<gr, 256, 0, st>>>(static_cast<double2*>(a), static_cast<double2*>(b), g,
+                                                          pa, pb, 0, 0, lo, hi);
+  else if (mode == MODE_VEC2)
+    k_exchange_masked<float4, false><<<gr, 256, 0, st>>>(static_cast<float4*>(a), static_cast<float4*>(b), g, pa,
+                                                         pb, 0, 0, lo, hi);
+  else
+    k_exchange_masked<float4, true><<<gr, 256, 0, st>>>(static_cast<float4*>(a), static_cast<float4*>(b), g, pa,
+                                                        pb, la, lb, lo, hi);
+  return cudaGetLastError();
+}
+
 template <typename V>
 __global__ void __launch_bounds__(256) k_exchange_all(V* __restrict__ a, V* __restrict__ b, uint64_t n) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;

@@ -9,9 +9,10 @@ on local bits; a global target is first swapped with a local "victim" bit.
 
 The reference stages full segment copies and scatters with per-amplitude
 index arrays (distsim.py:153-198).  Here a (global, local) swap is one
-in-place pass of the exchange kernel over each segment pair (peer access when
-the two segments sit on different GPUs), local pairs use the in-place bit
-swap kernel, and (global, global) pairs relabel whole segments without
+in-place pass of the masked exchange kernel per segment pair, all (global,
+local) pairs of one swap batched into 2^q - 1 rounds (shard.batched_exchange;
+peer access when the two segments sit on different GPUs, the work split
+between both), local pairs use the in-place bit swap kernel, and (global, global) pairs relabel whole segments without
 moving data.  TransferStats keeps the reference's accounting (closed form,
 see plan.py).  For the one-process-per-GPU layer see multigpu.py.
 """
@@ -36,6 +37,7 @@ from .plan import (
     swap_transfer,
 )
 from .mirror import mirror_of
+from .shard import batched_exchange, relabel_segments
 from .statevec import StateVector
 
 __all__ = ["Exchange", "ReorderPlan", "TransferStats", "SegmentedStateVector"]
@@ -187,16 +189,10 @@ class SegmentedStateVector:
         if dec.local_pairs:
             for st in self._devs:
                 st.swap_bits(dec.local_pairs)
-        for j, l in dec.global_local:
-            for s0 in range(nseg):
-                if not (s0 >> j) & 1:
-                    self._devs[s0].exchange_halves(self._devs[s0 | (1 << j)], l)
-        for j1, j2 in dec.global_global:
-            segs = list(self._devs)
-            for s in range(nseg):
-                if ((s >> j1) ^ (s >> j2)) & 1:
-                    segs[s] = self._devs[s ^ ((1 << j1) | (1 << j2))]
-            self._devs = segs
+        if dec.global_local:
+            batched_exchange(self._devs, dec.global_local)
+        if dec.global_global:
+            self._devs = relabel_segments(self._devs, dec.global_global, nseg)
         self._mutated()
         ex, moved, intra, inter = swap_transfer(pairs, self.local_bits, self.global_bits, self.workers)
         if ex:

@@ -6,12 +6,15 @@ GPU, distsim.py:69-277, made multi-process).
   a gate whose global control bits disagree with the rank's bits is skipped
   (distsim.py:232-244).
 * A global target is relocated first with the reference's victim rule
-  (plan.relocation_pairs).  The (global, local) index-bit swap is ONE
-  in-place pass of the exchange kernel over NVLink: each rank maps its
-  partner's segment through CUDA IPC and both ranks swap half of the
-  2^(n-g-1) exchanged amplitude pairs each, reading and writing both HBMs
-  directly (peer loads/stores, no staging buffer — 34q c128 on 2 GPUs leaves
-  no room for one).  No NCCL on amplitude data.
+  (plan.relocation_pairs; ties toward the highest local bit).  The (global,
+  local) pairs of one reorder run together as 2^q - 1 rounds of pairwise
+  masked exchanges (plan.exchange_rounds), each ONE in-place pass over
+  NVLink: each rank maps its partner's segment through CUDA IPC and both
+  ranks swap half of the exchanged amplitudes each, reading and writing both
+  HBMs directly (peer loads/stores, no staging buffer — 34q c128 on 2 GPUs
+  leaves no room for one).  No NCCL on amplitude data.  The torch-free
+  single-process engine (one host thread, all GPUs) is shard.py; this module
+  is the torchrun (one process per GPU) form.
 * Reductions (norm, marginals, Pauli expectations) reduce per rank on the
   GPU and all-reduce a handful of float64s through torch.distributed (NCCL
   on a GPU job, gloo on CPU tests).
@@ -31,8 +34,8 @@ import numpy as np
 
 from .core import InvalidArgumentError, check_swap_pairs
 from .gates import Gate, PauliString, PermutationGate
-from .plan import (TransferStats, decompose_swap, localize_phased, relabel, relocation_pairs, segment_selected,
-                   split_controls, swap_transfer)
+from .plan import (TransferStats, decompose_swap, exchange_rounds, initial_placement, localize_phased, relabel,
+                   relocation_pairs, segment_selected, split_controls, swap_transfer)
 
 
 class TorchComm:
@@ -137,15 +140,18 @@ class NvlinkSegment:
         self.seg.sync()
 
     # exchanges over NVLink (both partners call; each does half)
-    def exchange_halves(self, partner: int, local_bit: int, i_am_low: bool):
+    def exchange_masked(self, partner: int, lbits, pat_low: int, pat_high: int, i_am_low: bool):
+        """One round of a batched (global, local) swap between this rank and
+        `partner`: low[off | pat_low] <-> high[off | pat_high], each rank
+        running one half of the offsets over the peer mapping."""
         self.seg.sync()
         self.comm.barrier()
         peer = self._peer(partner)
         if i_am_low:
-            self.seg.exchange_halves(peer, local_bit, 0, 2)
+            self.seg.exchange_masked(peer, lbits, pat_low, pat_high, 0, 2)
             self.seg.sync()
         else:
-            peer.exchange_halves(self.seg, local_bit, 1, 2)
+            peer.exchange_masked(self.seg, lbits, pat_low, pat_high, 1, 2)
             peer.sync()
         self.comm.barrier()
 
@@ -193,38 +199,9 @@ class DistributedStateVector:
         self._basis0 = True
 
     def _place_for(self, gates) -> None:
-        """|0...0> is invariant under any relabelling of index bits, so before
-        the first gate the qubit map is free: put on the global bits the
-        qubits whose first use as a target comes last (never: first).  A QFT
-        then needs one global<->local reorder instead of two (no data moves
-        here: only the map changes)."""
-        n, nloc = self.num_qubits, self.local_bits
-        ng = n - nloc
-        first: dict[int, int] = {}
-        for i, g in enumerate(gates):
-            for q in getattr(g, "targets", ()):
-                first.setdefault(q, i)
-        never = [q for q in range(n) if q not in first]
-        glob = never[:ng]
-        if len(glob) < ng:
-            # the latest gate that first-targets enough qubits takes all the
-            # remaining global slots: one reorder brings them in together
-            need = ng - len(glob)
-            for i in range(len(gates) - 1, -1, -1):
-                fresh = [q for q in getattr(gates[i], "targets", ()) if first.get(q) == i and q not in glob]
-                if len(fresh) >= need:
-                    glob += sorted(fresh)[:need]
-                    break
-        if len(glob) < ng:  # fall back: qubits whose first use as a target comes last
-            order = sorted((q for q in range(n) if q not in glob), key=lambda q: (-first.get(q, len(gates) + 1), -q))
-            glob += order[: ng - len(glob)]
-        loc = [q for q in range(n) if q not in glob]
-        qmap = [0] * n
-        for b, q in enumerate(loc):
-            qmap[q] = b
-        for j, q in enumerate(sorted(glob)):
-            qmap[q] = nloc + j
-        self.qubit_map = qmap
+        """|0...0> is invariant under any relabelling of index bits: choose
+        the qubit map before the first gate (plan.initial_placement)."""
+        self.qubit_map = initial_placement(gates, self.num_qubits, self.local_bits)
 
     def distributed_index_bit_swap(self, pairs: Sequence[tuple[int, int]]) -> None:
         check_swap_pairs(pairs)
@@ -235,9 +212,11 @@ class DistributedStateVector:
         dec = decompose_swap(pairs, self.local_bits)
         if dec.local_pairs:
             self.seg.swap_bits(dec.local_pairs)
-        for j, l in dec.global_local:
-            partner = self.rank ^ (1 << j)
-            self.seg.exchange_halves(partner, l, i_am_low=not (self.rank >> j) & 1)
+        # all (global, local) pairs at once: 2^q - 1 rounds, every rank in
+        # exactly one pair per round (plan.exchange_rounds)
+        for _, s, t, lbits, pat_s, pat_t in exchange_rounds(dec.global_local, self.comm.world):
+            if self.rank in (s, t):
+                self.seg.exchange_masked(t if self.rank == s else s, lbits, pat_s, pat_t, i_am_low=self.rank == s)
         for j1, j2 in dec.global_global:
             if ((self.rank >> j1) ^ (self.rank >> j2)) & 1:
                 partner = self.rank ^ ((1 << j1) | (1 << j2))
@@ -264,7 +243,8 @@ class DistributedStateVector:
             return
         if len(g.targets) > self.local_bits:
             raise InvalidArgumentError(f"gate arity {len(g.targets)} exceeds local capacity {self.local_bits}")
-        pairs = relocation_pairs(self.qubit_map, self.local_bits, [self.qubit_map[q] for q in g.targets], upcoming)
+        pairs = relocation_pairs(self.qubit_map, self.local_bits, [self.qubit_map[q] for q in g.targets], upcoming,
+                                 prefer_high=True)
         if pairs:
             self.distributed_index_bit_swap(pairs)
         if isinstance(g, PhasedDenseGate):
@@ -313,7 +293,7 @@ class DistributedStateVector:
         total = 0.0 + 0.0j
         for pauli in paulis:
             flip = [self.qubit_map[q] for q, p in pauli.factors if p in "XY"]
-            pairs = relocation_pairs(self.qubit_map, self.local_bits, flip, [])
+            pairs = relocation_pairs(self.qubit_map, self.local_bits, flip, [], prefer_high=True)
             if pairs:
                 self.distributed_index_bit_swap(pairs)
             local, sign = [], 1.0

@@ -115,11 +115,14 @@ def relabel(qubit_map: list[int], pairs: Sequence[tuple[int, int]]) -> list[int]
 
 
 def relocation_pairs(qubit_map: Sequence[int], nloc: int, target_bits: Sequence[int],
-                     upcoming) -> list[tuple[int, int]]:
+                     upcoming, prefer_high: bool = False) -> list[tuple[int, int]]:
     """(global, local) swaps that make every target bit local
     (distsim.py:202-221): victims are local non-target bits whose qubit is
     next used as a target furthest in the future (never: first); ties go to
-    the lowest bit."""
+    the lowest bit — the reference's rule, which the drop-in
+    SegmentedStateVector keeps so its qubit_map matches.  The sharded engines
+    pass prefer_high=True: ties go to the HIGHEST local bit, so the exchange
+    moves long contiguous runs instead of every other amplitude."""
     need = [b for b in target_bits if b >= nloc]
     if not need:
         return []
@@ -132,7 +135,7 @@ def relocation_pairs(qubit_map: Sequence[int], nloc: int, target_bits: Sequence[
     cands = [b for b in range(nloc) if b not in target_bits]
     if len(need) > len(cands):
         raise InvalidArgumentError("gate arity exceeds local capacity")
-    cands.sort(key=lambda b: (-next_use.get(owner[b], horizon), b))
+    cands.sort(key=lambda b: (-next_use.get(owner[b], horizon), -b if prefer_high else b))
     return [(gb, cands[i]) for i, gb in enumerate(need)]
 
 
@@ -179,3 +182,61 @@ def localize_phased(op, qubit_map: Sequence[int], nloc: int, seg: int, dtype):
         elif (seg >> (bit - nloc)) & 1:
             m *= cmath.exp(1j * t)
     return m.astype(dtype), [qubit_map[q] for q in op.targets], cross, outside
+
+
+def initial_placement(gates, n: int, nloc: int) -> list[int]:
+    """Qubit map for a state that is still |0...0>: that state is invariant
+    under any relabelling of index bits, so before the first gate the map is
+    free.  Put on the global bits the qubits whose first use as a target comes
+    last (never: first), so e.g. a QFT needs one global<->local reorder
+    instead of two.  No data moves; only the map changes."""
+    ng = n - nloc
+    first: dict[int, int] = {}
+    for i, g in enumerate(gates):
+        for q in getattr(g, "targets", ()):
+            first.setdefault(q, i)
+    glob = [q for q in range(n) if q not in first][:ng]
+    if len(glob) < ng:
+        # the latest gate that first-targets enough qubits takes all the
+        # remaining global slots: one reorder brings them in together
+        need = ng - len(glob)
+        for i in range(len(gates) - 1, -1, -1):
+            fresh = [q for q in getattr(gates[i], "targets", ()) if first.get(q) == i and q not in glob]
+            if len(fresh) >= need:
+                glob += sorted(fresh)[:need]
+                break
+    if len(glob) < ng:  # fall back: qubits whose first use as a target comes last
+        order = sorted((q for q in range(n) if q not in glob), key=lambda q: (-first.get(q, len(gates) + 1), -q))
+        glob += order[: ng - len(glob)]
+    loc = [q for q in range(n) if q not in glob]
+    qmap = [0] * n
+    for b, q in enumerate(loc):
+        qmap[q] = b
+    for j, q in enumerate(sorted(glob)):
+        qmap[q] = nloc + j
+    return qmap
+
+
+def exchange_rounds(global_local: Sequence[tuple[int, int]], nseg: int):
+    """Schedule of a batched (global, local) swap of q pairs (j_i, l_i) over
+    nseg segments: round m (a nonzero q-bit mask) pairs every segment s with
+    t = s ^ M(m), M flipping the global bits j_i selected by m — a perfect
+    matching, so every segment works in every round.  Segment s sends t the
+    amplitudes whose local bits l_i equal t's bits j_i and receives those of t
+    whose l_i equal s's j_i:  a_s[off | pat(t)] <-> a_t[off | pat(s)].
+    Each amplitude moves at most once: a q-bit swap moves (1 - 2^-q) of the
+    vector in 2^q - 1 rounds instead of q/2 of it per pair done one by one.
+    Yields (round, s, t, lbits, pat_s_side, pat_t_side) with s < t."""
+    js = [j for j, _ in global_local]
+    ls = [l for _, l in global_local]
+    q = len(js)
+
+    def pat(seg: int) -> int:
+        return sum(((seg >> j) & 1) << l for j, l in zip(js, ls))
+
+    for m in range(1, 1 << q):
+        flip = sum(1 << js[i] for i in range(q) if (m >> i) & 1)
+        for s in range(nseg):
+            t = s ^ flip
+            if s < t:
+                yield m, s, t, ls, pat(t), pat(s)

@@ -112,9 +112,10 @@ class NumpySegment:
             dist.send(out, partner)
         return buf.numpy().view(self.dtype)
 
-    def exchange_halves(self, partner, l, i_am_low):
+    def exchange_masked(self, partner, lbits, pat_low, pat_high, i_am_low):
         idx = np.arange(self.a.size)
-        mine = idx[((idx >> l) & 1) == (1 if i_am_low else 0)]
+        mask = sum(1 << b for b in lbits)
+        mine = idx[(idx & mask) == (pat_low if i_am_low else pat_high)]
         self.a[mine] = self._sendrecv(partner, self.a[mine].astype(np.complex128), i_am_low).astype(self.dtype)
 
     def exchange_all(self, partner, i_am_low):
