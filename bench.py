@@ -239,6 +239,49 @@ def gate_payload_bytes(gates, itemsize: int) -> int:
     return b
 
 
+def qft33_check(st, step, ops, samples: int = 1 << 20) -> dict:
+    """Correctness of the timed workload at full size (64 GiB, no host copy
+    of the state): QFT|0> must be uniform 2^-16.5 and QFT|x> the DFT column
+    w^(x y) / sqrt(N), checked on 2^20 amplitudes read back from 16 spread
+    chunks (logical indices through the final bit_map), plus the norm and the
+    4-qubit marginals.  Bars: north_star max|d| <= 1e-5 absolute; also
+    reported relative to the 2^-16.5 amplitude scale."""
+    nat = st.native
+    n = N_QUBITS
+    N = 1 << n
+    chunk = samples // 16
+    begins = [int(b) for b in np.linspace(0, N - chunk, 16).astype(np.int64)]
+    out = {}
+    for tag, x in (("qft_zero", 0), ("qft_x", 0x1_2345_6789 % N)):
+        nat.set_basis(x)
+        st.bit_map = list(range(n))
+        for g in ops:
+            st.apply(g)
+        qubit_of_bit = [0] * n
+        for q, b in enumerate(st.bit_map):
+            qubit_of_bit[b] = q
+        err = 0.0
+        for b0 in begins:
+            a = nat.download(np.empty(chunk, np.complex64), b0, chunk).astype(np.complex128)
+            phys = np.arange(b0, b0 + chunk, dtype=np.uint64)
+            logical = np.zeros(chunk, dtype=np.uint64)
+            for b in range(n):
+                logical |= ((phys >> np.uint64(b)) & np.uint64(1)) << np.uint64(qubit_of_bit[b])
+            xy = (logical * np.uint64(x)) & np.uint64(N - 1)  # x*y mod 2^n (uint64 wraps mod 2^64)
+            want = np.exp(2j * np.pi * (xy.astype(np.float64) / N)) / np.sqrt(N)
+            err = max(err, float(np.abs(a - want).max()))
+        p = st.probabilities([0, 1, 2, 3])
+        out[tag] = {"x": x, "samples": samples, "max_abs_dev": err, "max_rel_dev": err * np.sqrt(N),
+                    "norm_dev": abs(st.norm_squared() - 1.0),
+                    "marginal_max_dev": float(np.abs(p - 1 / 16).max())}
+    ok = all(v["max_abs_dev"] <= 1e-5 and v["norm_dev"] <= 1e-5 for v in out.values())
+    out["pass"] = ok
+    if not ok:
+        print(json.dumps({"qft33_check": out}), file=sys.stderr, flush=True)
+        raise RuntimeError("QFT-33 result check failed")
+    return out
+
+
 def run_single(args) -> None:
     from paper_2308_01999_b200 import _native as N
     from paper_2308_01999_b200.statevec import StateVector
@@ -310,6 +353,7 @@ def run_single(args) -> None:
         nat.event_record(3)
         k6_ms.append(nat.event_elapsed(2, 3))
     k6_ms = min(k6_ms)
+    check = qft33_check(st, step, ops)
     del st, nat
 
     # e2e through the public API: fuse on the host, allocate, run, read back probabilities
@@ -373,6 +417,7 @@ def run_single(args) -> None:
         "gpu_launches": launches,
         "clocks": clk,
         "kernels": kernels,
+        "check": check,
     }
     print(json.dumps(line), flush=True)
 

@@ -275,6 +275,29 @@ def fam_misc(rng):
     return out
 
 
+def fam_config1(rng):
+    """BASELINE configs[0]: QFT-20 complex128 (runs on the reference as-is),
+    unfused (220 gates) and fused with FusionConfig(5, 6) (66 ops), from
+    |0...0> and from a seeded random state.  The 16 MiB states are not stored
+    whole: 8192 seeded amplitude samples, marginals and the norm are."""
+    n = 20
+    gates = to_gates(gen_qft(n))
+    fc = fuse(gates, FusionConfig(5, 6))
+    state_seed = 2020
+    st = random_state(n, np.random.default_rng(state_seed))
+    idx = np.sort(np.random.default_rng(2021).choice(1 << n, size=8192, replace=False))
+    out = {"n": n, "state_seed": state_seed, "idx": idx, "gates": len(gates), "fused_ops": len(fc.gates)}
+    for tag, start in (("zero", None), ("random", st)):
+        for ftag, gl in (("unfused", gates), ("fused", fc.gates)):
+            sv = StateVector.from_amplitudes(start) if start is not None else StateVector(n)
+            for g in gl:
+                sv.apply(g)
+            a = sv.logical_amplitudes()
+            out[f"{tag}_{ftag}"] = {"samples": a[idx].copy(), "norm": float(np.vdot(a, a).real),
+                                    "marginal_0_19_7_13": sv.probabilities([0, 19, 7, 13]).copy()}
+    return out
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     fams = {
@@ -285,8 +308,12 @@ def main():
         "fusion": fam_fusion,
         "distsim": fam_distsim,
         "misc": fam_misc,
+        "config1": fam_config1,
     }
+    only = sys.argv[1:]
     for i, (name, fn) in enumerate(fams.items()):
+        if only and name not in only:
+            continue
         data = fn(np.random.default_rng(20261017 + i))
         meta = {"generator": "oracle/gen_golden.py", "reference": str(REF_SRC),
                 "numpy": np.__version__, "family": name}

@@ -53,6 +53,38 @@ def gate_from_spec(spec):
     return G.DenseGate(spec["matrix"], spec["targets"], spec["controls"], unitary=spec.get("unitary", True))
 
 
+# north_star parity bars (BASELINE.json): max |d amplitude| <= 1e-5 (c64) /
+# 1e-12 (c128) and fidelity >= 1 - 1e-6.  Normalised random states have
+# |a| ~ 2^(-n/2), so the absolute bar alone is loose at n >= 10: the error is
+# also bounded RELATIVE to the largest amplitude — 5e-5 for complex64 (fp32
+# accumulation over up to ~150 fused windows; the int8-digit tensor path
+# measures 1.6e-5 after 100 k = 5 windows, while a 1-pass TF32 or bf16
+# product is above 1e-4 after ONE gate) and 1e-12 for complex128.
+ABS_TOL = {np.dtype(np.complex64): 1e-5, np.dtype(np.complex128): 1e-12}
+REL_TOL = {np.dtype(np.complex64): 5e-5, np.dtype(np.complex128): 1e-12}
+FID_TOL = {np.dtype(np.complex64): 1e-6, np.dtype(np.complex128): 1e-12}
+
+
+def fidelity(a, b) -> float:
+    a = np.asarray(a, dtype=np.complex128).ravel()
+    b = np.asarray(b, dtype=np.complex128).ravel()
+    return float(abs(np.vdot(a, b)) ** 2 / (np.vdot(a, a).real * np.vdot(b, b).real))
+
+
+def assert_state_close(got, want, dtype, fid=True):
+    """|d| <= ABS_TOL, |d| <= REL_TOL * max|want|, fidelity >= 1 - FID_TOL."""
+    dt = np.dtype(dtype)
+    got = np.asarray(got)
+    want = np.asarray(want)
+    err = float(np.abs(got.astype(np.complex128) - want.astype(np.complex128)).max()) if got.size else 0.0
+    scale = float(np.abs(want).max()) if want.size else 0.0
+    assert err <= ABS_TOL[dt], f"max|d| {err:.3e} > {ABS_TOL[dt]:.0e}"
+    assert err <= REL_TOL[dt] * max(scale, 1e-300), f"max|d| {err:.3e} > {REL_TOL[dt]:.0e} x max|want| {scale:.3e}"
+    if fid and scale > 0:
+        f = fidelity(got, want)
+        assert f >= 1 - FID_TOL[dt], f"fidelity 1 - {1 - f:.3e}"
+
+
 def random_state(n: int, rng: np.random.Generator, dtype=np.complex128) -> np.ndarray:
     v = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
     return (v / np.linalg.norm(v)).astype(dtype)

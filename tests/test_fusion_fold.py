@@ -5,7 +5,7 @@ against the same oracle."""
 import numpy as np
 import pytest
 
-from conftest import random_state
+from conftest import assert_state_close, random_state
 from oracle import sv_oracle as O
 from paper_2308_01999_b200 import gates as G
 from paper_2308_01999_b200.circuits import gen_qaoa_maxcut, gen_qft, gen_qv, random_gate_sequence, to_gates
@@ -101,8 +101,7 @@ def test_fold_ops_on_gpu_match_oracle(dtype, name, n, make, gpu_available):
         sv = StateVector.from_amplitudes(st)
         for op in fc.ops:
             sv.apply(op)
-        tol = 2e-5 if dtype == np.complex64 else 1e-12
-        np.testing.assert_allclose(sv.logical_amplitudes(), want, atol=tol)
+        assert_state_close(sv.logical_amplitudes(), want, dtype)
 
 
 @pytest.mark.gpu

@@ -11,7 +11,7 @@ size-independent properties (SURVEY.md §7.3 hard part 4):
 import numpy as np
 import pytest
 
-from conftest import random_state
+from conftest import assert_state_close, random_state
 from oracle import sv_oracle as O
 from paper_2308_01999_b200 import gates as G
 from paper_2308_01999_b200.circuits import gen_qft, random_gate_sequence, to_gates
@@ -67,11 +67,10 @@ def test_large_round_trip_and_norm(dtype, n):
     start = sv.native.download()
     for g in gates:
         sv.apply(g)
-    assert abs(sv.norm_squared() - 1.0) < (1e-4 if dtype == np.complex64 else 1e-10)
+    assert abs(sv.norm_squared() - 1.0) < (1e-5 if dtype == np.complex64 else 1e-12)
     for g in reversed(gates):
         sv.apply(_dagger(g))
-    tol = 2e-5 if dtype == np.complex64 else 1e-12
-    assert np.abs(sv.native.download() - start).max() < tol
+    assert_state_close(sv.native.download(), start, dtype)
 
 
 def test_qft_uniform_at_26_qubits_fused():
@@ -93,8 +92,7 @@ def test_oracle_parity_at_22_qubits(dtype):
     sv = StateVector.from_amplitudes(st)
     for g in gates:
         sv.apply(g)
-    tol = 1e-5 if dtype == np.complex64 else 1e-12
-    np.testing.assert_allclose(sv.native.download(), want, atol=tol, rtol=0)
+    assert_state_close(sv.native.download(), want, dtype)
 
 
 def test_diagonal_bit_exact_at_24_qubits():
@@ -120,7 +118,7 @@ def test_segmented_equals_single_segment(gbits):
         ssv.run(gates)
         got = ssv.to_statevector().amplitudes
         assert ssv.stats.num_reorders > 0
-    np.testing.assert_allclose(got, ref, atol=1e-12)
+    assert_state_close(got, ref, np.complex128)
 
 
 def test_segmented_fold_ops_match_single():

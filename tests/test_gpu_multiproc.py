@@ -70,7 +70,7 @@ def test_ipc_exchange_multiprocess(world, dtype, gpu_available):
     for p in procs:
         p.join(timeout=60)
     assert "error" not in res, res
-    tol = 1e-12 if dtype == "complex128" else 2e-5
+    tol = 1e-12 if dtype == "complex128" else 1e-5
     assert res["state_err"] < tol
     assert res["prob_err"] < tol
     assert res["ev_err"] < tol

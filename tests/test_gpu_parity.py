@@ -8,7 +8,7 @@ max|d| <= 1e-5 (complex64) / 1e-12 (complex128)."""
 import numpy as np
 import pytest
 
-from conftest import gate_from_spec, golden, random_state
+from conftest import assert_state_close, gate_from_spec, golden, random_state
 from oracle import sv_oracle as O
 from paper_2308_01999_b200 import _native as N
 from paper_2308_01999_b200 import gates as G
@@ -211,7 +211,7 @@ def _check(got, want, dtype, exact):
     if exact:
         np.testing.assert_array_equal(got, want)
     else:
-        np.testing.assert_allclose(got, want, atol=TOL[np.dtype(dtype)] * 10, rtol=0)
+        assert_state_close(got, want, dtype)
 
 
 @pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
@@ -376,14 +376,14 @@ def test_reductions_vs_oracle(dtype):
             fac = tuple((int(q), str(rng.choice(list("IXYZ")))) for q in rng.permutation(n)[:m])
             got = sv.expectation([G.PauliString(fac)])
             want = O.expectation_pauli(st.astype(np.complex128), n, fac)
-            assert abs(got - want) < 1e-5
+            assert abs(got - want) <= TOL[np.dtype(dtype)]
         for kd in range(1, min(n, 6) + 1):
             tq = tuple(int(q) for q in rng.permutation(n)[:kd])
             a = rng.standard_normal((1 << kd, 1 << kd)) + 1j * rng.standard_normal((1 << kd, 1 << kd))
             herm = (a + a.conj().T) / 2
             got = sv.expectation(G.DenseGate(herm, tq, unitary=False))
             want = O.expectation_dense(st.astype(np.complex128), n, herm, tq)
-            assert abs(got - want) < 1e-4 * max(1.0, abs(want))
+            assert abs(got - want) <= TOL[np.dtype(dtype)] * max(1.0, abs(want))
         np.testing.assert_array_equal(sv.amplitudes, st)
 
 
@@ -400,7 +400,7 @@ def test_rotations_and_collapse_vs_oracle(dtype):
             sv.apply_pauli_rotation(theta, G.PauliString(fac, coef))
             want = st.copy()
             O.pauli_rotation(want, n, theta, fac, coef)
-            np.testing.assert_allclose(sv.amplitudes, want, atol=10 * TOL[np.dtype(dtype)])
+            assert_state_close(sv.amplitudes, want, dtype)
         k = int(rng.integers(1, min(n, 4) + 1))
         bits = rng.permutation(n)[:k].tolist()
         r = float(rng.random())
@@ -408,7 +408,7 @@ def test_rotations_and_collapse_vs_oracle(dtype):
         got = sv.measure(bits, r)
         want_o, want = O.measure(st, n, bits, r)
         assert got == want_o
-        np.testing.assert_allclose(sv.amplitudes, want, atol=10 * TOL[np.dtype(dtype)])
+        assert_state_close(sv.amplitudes, want, dtype, fid=False)
 
 
 def test_edge_cases_and_errors():

@@ -99,3 +99,24 @@ def test_bit_permute_naive(pairs):
         assert O.bit_permute_naive(int(x), m["pairs"]) == y
     for x in range(1 << 10):
         assert bit_permute(x, pairs) == O.bit_permute_naive(x, pairs)
+
+
+def test_config1_qft20_matches_reference():
+    """BASELINE config 1 (QFT-20 complex128, unfused 220 gates and fused
+    (5, 6) 66 ops) from |0> and a seeded random state: the oracle reproduces
+    the reference's sampled amplitudes, marginals and norm."""
+    from conftest import random_state
+    from paper_2308_01999_b200.circuits import gen_qft, to_gates
+    from paper_2308_01999_b200.fusion import FusionConfig, fuse
+
+    c = golden("config1")
+    n = c["n"]
+    gates = to_gates(gen_qft(n))
+    fused = fuse(gates, FusionConfig(5, 6)).gates
+    for start in ("zero", "random"):
+        st = random_state(n, np.random.default_rng(c["state_seed"])) if start == "random" else None
+        for tag, ops in (("unfused", gates), ("fused", fused)):
+            a = O.run_circuit(ops, n, state=st)
+            ref = c[f"{start}_{tag}"]
+            assert np.abs(a[c["idx"]] - ref["samples"]).max() <= 1e-13
+            np.testing.assert_allclose(O.marginal(a, n, [0, 19, 7, 13]), ref["marginal_0_19_7_13"], atol=1e-13)
