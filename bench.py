@@ -152,29 +152,86 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows), "samples_under_load": len(sm)}
 
 
-# ---- CPU baseline (the oracle port; checker code, timed beside the GPU) -----------------------
+# ---- CPU baseline: the reference itself (baseline/_ref), else the oracle port ------------------
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _reference_api():
+    """The UNMODIFIED reference package installed by tools/install_reference.sh
+    into baseline/_ref (git-ignored; it travels to the GPU box with the
+    snapshot).  Returns (statevec, fusion, circuits) modules, or None."""
+    if not (REF_DIR / "duetsim" / "__init__.py").exists():
+        return None
+    if "duetsim" in sys.modules and str(REF_DIR) not in str(getattr(sys.modules["duetsim"], "__file__", "")):
+        return None  # the repo's drop-in shim is already imported in this process
+    sys.path.insert(0, str(REF_DIR))
+    import duetsim  # noqa: F401
+    from duetsim import circuits, fusion, statevec
+
+    assert str(REF_DIR) in duetsim.__file__, duetsim.__file__
+    return statevec, fusion, circuits
+
+
+def host_info() -> dict:
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["threadpools"] = [{k: d.get(k) for k in ("internal_api", "num_threads", "version")}
+                               for d in threadpool_info()]
+    except Exception:  # pragma: no cover - optional
+        pass
+    return info
+
 
 def cpu_sample(nq: int, max_ops: int | None = None) -> dict:
-    """Time the NumPy restatement of the reference algorithm on QFT-nq fused
-    (5,6) and extrapolate to the 33-qubit workload: per-op time x 2^(33-nq)
-    x 152 ops (streaming cost is linear in 2^n beyond the CPU caches)."""
-    from oracle import sv_oracle as O
-    from paper_2308_01999_b200.circuits import gen_qft, to_gates
-    from paper_2308_01999_b200.fusion import FusionConfig, fuse
+    """Time the reference CPU path on QFT-nq fused with FusionConfig(5, 6)
+    (complex64) and extrapolate to the 33-qubit workload: per-op time
+    x 2^(33-nq) x 152 ops (streaming cost is linear in 2^n beyond the CPU
+    caches).  The reference package itself when installed (kind
+    "reference"), otherwise the oracle's NumPy restatement ("port")."""
+    api = _reference_api()
+    if api is not None:
+        statevec, fusion, circuits = api
+        gates = circuits.to_gates(circuits.gen_qft(nq))
+        fc = fusion.fuse(gates, fusion.FusionConfig(*FUSION))
+        ops = fc.gates if max_ops is None else fc.gates[:max_ops]
+        sv = statevec.StateVector(nq, dtype=np.complex64)
+        t0 = time.perf_counter()
+        for g in ops:
+            sv.apply(g)
+        dt = time.perf_counter() - t0
+        kind = "reference"
+    else:
+        from oracle import sv_oracle as O
+        from paper_2308_01999_b200.circuits import gen_qft, to_gates
+        from paper_2308_01999_b200.fusion import FusionConfig, fuse
 
-    fc = fuse(to_gates(gen_qft(nq)), FusionConfig(*FUSION))
-    ops = fc.gates if max_ops is None else fc.gates[:max_ops]
-    amps = np.zeros(1 << nq, dtype=np.complex64)
-    amps[0] = 1
-    t0 = time.perf_counter()
-    for g in ops:
-        O.apply_gate(amps, nq, g)
-    dt = time.perf_counter() - t0
+        gates = to_gates(gen_qft(nq))
+        fc = fuse(gates, FusionConfig(*FUSION))
+        ops = fc.gates if max_ops is None else fc.gates[:max_ops]
+        amps = np.zeros(1 << nq, dtype=np.complex64)
+        amps[0] = 1
+        t0 = time.perf_counter()
+        for g in ops:
+            O.apply_gate(amps, nq, g)
+        dt = time.perf_counter() - t0
+        kind = "port"
     per_op = dt / len(ops)
-    _, ops33, _ = workload("reference")
-    t33 = per_op * (1 << (N_QUBITS - nq)) * len(ops33)
+    n33_ops = 152  # FusionConfig(5, 6) windows of QFT-33 (SURVEY.md Appendix A)
+    t33 = per_op * (1 << (N_QUBITS - nq)) * n33_ops
     return {"value": 577.0 / t33, "unit": "gates/s", "seconds": dt, "ops": len(ops), "per_op_s": per_op,
-            "t33_s": t33}
+            "t33_s": t33, "kind": kind, "circuit_gates": len(gates),
+            "unextrapolated_gates_per_s": (len(gates) / dt) if max_ops is None else None}
 
 
 def cpu_cores() -> int:
@@ -184,31 +241,36 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+def _cpu_desc(r: dict, nq: int) -> str:
+    who = ("the unmodified reference (baseline/_ref duetsim: fuse + StateVector.apply)" if r["kind"] == "reference"
+           else "oracle port (NumPy restatement of statevec.py)")
+    return (f"{who} on the full QFT-{nq} fused(5,6) circuit ({r['ops']} ops, {r['seconds']:.1f} s, c64, "
+            f"{r['circuit_gates']} circuit gates -> {r['unextrapolated_gates_per_s'] or 0:.1f} gates/s at n={nq}); "
+            f"per-op time scaled x2^{N_QUBITS - nq} and x152 ops to QFT-33 (extrapolated: {r['t33_s']:.0f} s "
+            f"per circuit)")
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    os.environ.pop("OPENBLAS_NUM_THREADS", None)
-    ops_per_step = 16
-    for _ in range(args.warmup):
-        cpu_sample(CPU_SAMPLE_QUBITS, ops_per_step)
-    vals, secs = [], []
-    for _ in range(args.steps):
-        r = cpu_sample(CPU_SAMPLE_QUBITS, ops_per_step)
-        vals.append(r["value"])
-        secs.append(r["seconds"])
-    v = statistics.median(vals)
-    sample = (f"oracle port (NumPy restatement of statevec.py raw kernels) on the first {ops_per_step} fused ops of "
-              f"QFT-{CPU_SAMPLE_QUBITS} (5,6), c64; per-op time scaled x2^{N_QUBITS - CPU_SAMPLE_QUBITS} and x152 ops "
-              f"to QFT-33 (extrapolated)")
+    os.environ.pop("OPENBLAS_NUM_THREADS", None)  # BLAS on every core, as the reference runs by default
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_sample(CPU_SAMPLE_QUBITS)
+    rs = [cpu_sample(CPU_SAMPLE_QUBITS) for _ in range(args.steps)]
+    v = statistics.median(r["value"] for r in rs)
+    r0 = sorted(rs, key=lambda r: r["value"])[len(rs) // 2]
     line = {
         "metric": METRIC, "value": v, "unit": "gates/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "c64", "data": "synthetic (QFT circuit from |0>)",
+        "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(r["seconds"] for r in rs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c64",
+        "data": "synthetic (QFT circuit from |0>)",
         "config": {"workload": "qft33_c64_fused_k5", "n_qubits": N_QUBITS,
-                   "fusion": f"reference FusionConfig{FUSION} (the reference's own fuser)"},
+                   "fusion": f"reference FusionConfig{FUSION} (the reference's own fuser)",
+                   "sample": f"QFT-{CPU_SAMPLE_QUBITS}, every fused op, per step"},
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "gates/s", "cores": cpu_cores(), "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "gates/s", "cores": cpu_cores(), "kind": r0["kind"],
+                         "sample": _cpu_desc(r0, CPU_SAMPLE_QUBITS), "host": host_info()},
         "e2e": {"value": v, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -385,11 +447,8 @@ def run_single(args) -> None:
     if not args.skip_cpu:
         os.environ.pop("OPENBLAS_NUM_THREADS", None)
         r = cpu_sample(CPU_SAMPLE_QUBITS)
-        cpu = {"value": r["value"], "unit": "gates/s", "cores": cpu_cores(), "kind": "port",
-               "sample": (f"oracle port (NumPy restatement of statevec.py) on the full QFT-{CPU_SAMPLE_QUBITS} "
-                          f"fused(5,6) circuit ({r['ops']} ops, {r['seconds']:.1f} s, c64); per-op time scaled "
-                          f"x2^{N_QUBITS - CPU_SAMPLE_QUBITS} and x152 ops to QFT-33 (extrapolated: "
-                          f"{r['t33_s']:.0f} s per circuit)")}
+        cpu = {"value": r["value"], "unit": "gates/s", "cores": cpu_cores(), "kind": r["kind"],
+               "sample": _cpu_desc(r, CPU_SAMPLE_QUBITS)}
 
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": 1, "steps": args.steps,

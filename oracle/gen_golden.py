@@ -298,6 +298,38 @@ def fam_config1(rng):
     return out
 
 
+def fam_cli(rng):
+    """The reference CLI's `simulate` reports (cli.py:124-244), timings
+    dropped: digests, norms, counters and transfer stats that the GPU CLI
+    must reproduce for the same arguments."""
+    import contextlib
+    import io
+    import json
+
+    from duetsim.cli import main as ref_main
+
+    runs = [
+        ["simulate", "--circuit", "qft", "--n", "10"],
+        ["simulate", "--circuit", "qft", "--n", "12", "--max-fused-gate-size", "4",
+         "--max-fused-diagonal-gate-size", "6"],
+        ["simulate", "--circuit", "qft", "--n", "10", "--engine", "sv-dist", "--global-bits", "2", "--workers", "2"],
+        ["simulate", "--circuit", "qv", "--n", "8", "--seed", "5", "--verify"],
+        ["simulate", "--circuit", "qaoa", "--n", "6", "--engine", "sv-dist", "--global-bits", "1", "--verify"],
+        ["simulate", "--circuit", "qft", "--n", "20", "--verify"],
+    ]
+    out = []
+    for argv in runs:
+        buf, err = io.StringIO(), io.StringIO()
+        with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(err):
+            code = ref_main(argv)
+        rep = json.loads(buf.getvalue()) if buf.getvalue().strip() else None
+        if rep is not None:
+            rep.pop("timings", None)
+        out.append({"argv": argv, "code": code, "report": rep,
+                    "stderr": json.loads(err.getvalue()) if err.getvalue().strip() else None})
+    return out
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     fams = {
@@ -309,6 +341,7 @@ def main():
         "distsim": fam_distsim,
         "misc": fam_misc,
         "config1": fam_config1,
+        "cli": fam_cli,
     }
     only = sys.argv[1:]
     for i, (name, fn) in enumerate(fams.items()):

@@ -3,10 +3,20 @@ engines, mirroring the reference's ``duetsim simulate``
 (cli.py:124-244) — same flags, same JSON report schema (schema_version,
 command, engine, params, counters, digest, verification, timings; timing
 fields isolated under "timings" so reports compare equal modulo timings) and
-exit codes (0 ok, 2 verification failure) — extended with what the GPU engine
-adds: ``--dtype``, ``--fusion fold:K`` (the phase-folding fuser), ``--device``
-and, in the report, per-kernel-class device times, algorithmic HBM bytes and
-achieved GB/s.
+exit codes (0 ok, 2 verification failure or invalid argument, with
+``{"error": "invalid-argument", "detail": ...}`` on stderr as in the
+reference's cli.py:601-610; ``--workers`` defaults to $DUETSIM_WORKERS,
+cli.py:53-54) — extended with what the GPU engine adds: ``--dtype``,
+``--fusion fold:K`` (the phase-folding fuser), ``--device``, ``--gpus N``
+(the state sharded over N GPUs by one host process, shard.py) and, in the
+report, per-kernel-class device times, algorithmic HBM bytes and achieved
+GB/s.
+
+``--verify`` follows the reference (cli.py:120-122, :187-210): the result is
+compared with the UNFUSED circuit run by the state-vector engine in
+complex128 — here that run takes the 1-/2-qubit CUDA-core kernels while the
+fused / folded / sharded run under test takes the window and tensor-core
+kernels and the exchanges.
 
     python -m paper_2308_01999_b200.cli simulate --circuit qft --n 30 --dtype c64 --fusion fold:5
 
@@ -19,6 +29,7 @@ from __future__ import annotations
 import argparse
 import hashlib
 import json
+import os
 import sys
 import time
 
@@ -35,6 +46,12 @@ EXIT_OK = 0
 EXIT_VERIFY = 2
 DTYPES = {"c64": np.complex64, "c128": np.complex128}
 STREAM_QUBITS = 26  # above this the report's digest and norm are streamed chunk by chunk
+VERIFY_MAX_QUBITS = 20  # the reference stops at 14 (cli.py:188); the GPU engine verifies up to 20
+
+
+def default_workers() -> int:
+    """Worker count default, as the reference's cli.py:53-54."""
+    return int(os.environ.get("DUETSIM_WORKERS", "1"))
 
 
 def digest_array(arr: np.ndarray) -> str:
@@ -124,8 +141,31 @@ def cmd_simulate(args) -> int:
         emit(report, args.out)
         return EXIT_OK
 
+    if args.verify and n > VERIFY_MAX_QUBITS:
+        raise InvalidArgumentError(f"--verify limited to n <= {VERIFY_MAX_QUBITS}")
+    if args.gpus < 1:
+        raise InvalidArgumentError("--gpus must be >= 1")
     ops = fused_ops(args, to_gates(circuit), counters, timings)
-    if args.engine == "sv":
+    if args.engine == "sv" and args.gpus > 1:
+        from . import _native as N
+        from .shard import ShardedStateVector
+
+        ndev = max(1, N.device_count())
+        devices = [d % ndev for d in range(args.gpus)]
+        t0 = time.perf_counter()
+        sh = ShardedStateVector(n, devices, dtype)
+        timings["alloc_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sh.prof(True)
+        sh.run(ops)
+        sh.sync()
+        timings["apply_s"] = time.perf_counter() - t0
+        counters.update(_kernel_report(sh.prof_read(), timings["apply_s"]))
+        counters["transfer_stats"] = sh.stats.as_dict()
+        params["gpus"] = args.gpus
+        amps = sh.gather_logical()
+        sh.close()
+    elif args.engine == "sv":
         t0 = time.perf_counter()
         sv = StateVector(n, dtype=dtype, device=args.device)
         sv.native.sync()
@@ -159,7 +199,13 @@ def cmd_simulate(args) -> int:
         amps = sv.logical_amplitudes()
     else:
         t0 = time.perf_counter()
-        with SegmentedStateVector(n, args.global_bits, args.workers, dtype=dtype) as ssv:
+        devices = None
+        if args.gpus > 1:
+            from . import _native as N
+
+            devices = [d % max(1, N.device_count()) for d in range(args.gpus)]
+            params["gpus"] = args.gpus
+        with SegmentedStateVector(n, args.global_bits, args.workers, dtype=dtype, devices=devices) as ssv:
             segs = ssv.native_segments
             for s in segs:
                 s.prof_enable(True)
@@ -176,8 +222,6 @@ def cmd_simulate(args) -> int:
 
     verification = None
     if args.verify:
-        if n > 20:
-            raise InvalidArgumentError("--verify limited to n <= 20")
         # the unfused circuit in complex128 on the same engine (the reference
         # verifies against its own run_circuit_sv the same way, cli.py:120-122)
         t0 = time.perf_counter()
@@ -216,12 +260,13 @@ def build_parser() -> argparse.ArgumentParser:
     sim.add_argument("--p", type=int, default=2)
     sim.add_argument("--engine", choices=["sv", "sv-dist", "mps", "tn"], default="sv")
     sim.add_argument("--global-bits", type=int, default=1)
-    sim.add_argument("--workers", type=int, default=1)
+    sim.add_argument("--workers", type=int, default=default_workers())
     sim.add_argument("--max-fused-gate-size", type=int, default=None)
     sim.add_argument("--max-fused-diagonal-gate-size", type=int, default=None)
     sim.add_argument("--fusion", default=None, help="fold:K — the phase-folding fuser with K-qubit windows")
     sim.add_argument("--dtype", choices=sorted(DTYPES), default="c128")
     sim.add_argument("--device", type=int, default=None)
+    sim.add_argument("--gpus", type=int, default=1, help="shard the state over N GPUs (one host process)")
     sim.add_argument("--verify", action="store_true")
     sim.add_argument("--dry-run", action="store_true")
     sim.set_defaults(func=cmd_simulate)
@@ -233,8 +278,8 @@ def main(argv=None) -> int:
     try:
         return args.func(args)
     except InvalidArgumentError as e:
-        print(json.dumps({"error": str(e)}), file=sys.stderr)
-        return 1
+        print(json.dumps({"error": "invalid-argument", "detail": str(e)}), file=sys.stderr)
+        return EXIT_VERIFY
 
 
 if __name__ == "__main__":

@@ -277,13 +277,15 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   coop_phase(1, tq[1]);
   cp_async_wait<S - 2>();  // tile 0 landed (this thread's part; the barrier below publishes it)
 
-  if (*tmem_slot != 0u) __trap();  // whole-TMEM allocation starts at lane 0, column 0
   const uint32_t tmem = uint32_t(grp * 256);
   const uint32_t tlane = tmem + (uint32_t((warp & 3) * 32) << 16);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B operand: generic -> async proxy
   fence_before();
   __syncthreads();
   fence_after();
+  // read only after the barrier: warp 0's tcgen05.alloc wrote the slot
+  // (compute-sanitizer racecheck flagged the earlier pre-barrier read)
+  if (*tmem_slot != 0u) __trap();  // whole-TMEM allocation starts at lane 0, column 0
 
   // out = 2^(e_row + e_b - 16) (acc0 + acc12 / 2^8); columns 2i (re), 2i+1 (im).
   // Lanes 2t', 2t'+1 hold adjacent amplitudes: they swap one member per pair

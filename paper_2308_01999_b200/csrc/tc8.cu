@@ -265,12 +265,14 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
   if (PHASED && !p.coop) row_angles(tq[0] | rowoff);
   cp_async_wait<S - 2>();
 
-  if (*tmem_slot != 0u) __trap();
   const uint32_t tlane = uint32_t(grp * 256) + (uint32_t((warp & 3) * 32) << 16);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   fence_before();
   __syncthreads();
   fence_after();
+  // read only after the barrier: warp 0's tcgen05.alloc wrote the slot
+  // (compute-sanitizer racecheck flagged the earlier pre-barrier read)
+  if (*tmem_slot != 0u) __trap();  // whole-TMEM allocation starts at lane 0, column 0
 
   // out = scale (hi 2^16 + mid 2^8 + lo): the accumulators read back as
   // M + acc (M = 1.5 * 2^23); t2 = V + 257 M, removed by the last fma

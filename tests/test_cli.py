@@ -29,7 +29,26 @@ def test_qft_33_dry_run(capsys):
 
 
 def test_out_of_scope_engine_is_an_error(capsys):
-    assert main(["simulate", "--circuit", "qft", "--n", "4", "--engine", "mps"]) == 1
+    assert main(["simulate", "--circuit", "qft", "--n", "4", "--engine", "mps"]) == 2
+    err = json.loads(capsys.readouterr().err)
+    assert err["error"] == "invalid-argument" and "mps" in err["detail"]
+
+
+def test_invalid_argument_exit_code_and_json(capsys):
+    """The reference prints {"error": "invalid-argument", "detail": ...} and
+    exits 2 (cli.py:606-610); --verify limits are checked before any work."""
+    assert main(["simulate", "--circuit", "qft", "--n", "30", "--verify"]) == 2
+    err = json.loads(capsys.readouterr().err)
+    assert err == {"error": "invalid-argument", "detail": "--verify limited to n <= 20"}
+    assert main(["simulate", "--circuit", "qft", "--n", "4", "--gpus", "0"]) == 2
+
+
+def test_workers_default_from_environment(monkeypatch):
+    from paper_2308_01999_b200.cli import build_parser
+
+    monkeypatch.setenv("DUETSIM_WORKERS", "3")
+    args = build_parser().parse_args(["simulate", "--circuit", "qft", "--n", "4"])
+    assert args.workers == 3
 
 
 @pytest.mark.gpu
@@ -91,3 +110,37 @@ class TestSimulateGPU:
         _, streamed = run_json(capsys, *args)
         assert streamed["digest"] == full["digest"]
         assert abs(streamed["counters"]["norm"] - full["counters"]["norm"]) < 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", range(5))
+def test_reports_match_the_reference_cli(capsys, case, gpu_available):
+    """The GPU CLI against the reference CLI's own reports for the same
+    arguments (tests/golden/cli.pkl.gz, made by oracle/gen_golden.py):
+    counters (gates, fused_gates, transfer_stats), exit code, verification,
+    the norm to 1e-12 and — for QFT from |0>, whose rounded amplitudes sit
+    far from rounding boundaries — the digest itself."""
+    from conftest import golden
+
+    ref = golden("cli")[case]
+    code, rep = run_json(capsys, *ref["argv"])
+    assert code == ref["code"]
+    want = ref["report"]
+    for key in ("gates", "fused_gates", "transfer_stats"):
+        assert rep["counters"].get(key) == want["counters"].get(key), key
+    assert abs(rep["counters"]["norm"] - want["counters"]["norm"]) <= 1e-12
+    if "qft" in ref["argv"]:
+        assert rep["digest"] == want["digest"]
+    if want.get("verification") is not None:
+        assert rep["verification"]["passed"] == want["verification"]["passed"]
+        assert rep["verification"]["max_error"] <= 1e-10
+
+
+@pytest.mark.gpu
+def test_gpus_flag_shards_and_verifies(capsys, gpu_available):
+    code, rep = run_json(capsys, "simulate", "--circuit", "qv", "--n", "12", "--dtype", "c128", "--gpus", "4",
+                         "--verify")
+    assert code == 0
+    assert rep["verification"]["passed"]
+    assert rep["params"]["gpus"] == 4
+    assert rep["counters"]["transfer_stats"]["num_reorders"] > 0
