@@ -415,6 +415,35 @@ def run_single(args) -> None:
         nat.event_record(3)
         k6_ms.append(nat.event_elapsed(2, 3))
     k6_ms = min(k6_ms)
+    # the same circuit on the fp32-level bf16-limb tensor kernels (tc.cu,
+    # DSV_TC8=0): the int8-digit default drops the digit products below 2^16
+    N.config_set("tc8", 0)
+    step()
+    nat.event_record(2)
+    step()
+    nat.event_record(3)
+    tc_ms = nat.event_elapsed(2, 3)
+    N.config_set("tc8", 1)
+    # generic states (random amplitudes keep the tensor kernels busier and can
+    # trip sw_power_cap): quantum volume depth 30 fold-fused at k = 5, and
+    # config 5's random 1-/2-qubit generator unfused, both at n = 33 c64
+    from paper_2308_01999_b200.circuits import gen_qv, random_gate_sequence, to_gates
+
+    legs = {}
+    clocks2 = ClockSampler(dev).start()
+    time.sleep(0.2)
+    qv_gates = to_gates(gen_qv(N_QUBITS, 30, seed=0))
+    qv_ops = fuse_fold(qv_gates, FOLD_K).ops
+    rnd = random_gate_sequence(N_QUBITS, 200, np.random.default_rng(0), max_arity=2)
+    for name, circ, lops in (("qv33_c64_fold5", qv_gates, qv_ops), ("random33_c64", rnd, rnd)):
+        step(lops)
+        nat.event_record(2)
+        step(lops)
+        nat.event_record(3)
+        ms = nat.event_elapsed(2, 3)
+        legs[name] = {"gates_per_s": len(circ) / (ms / 1000.0), "ms_per_circuit": ms, "circuit_gates": len(circ),
+                      "ops": len(lops), "norm_dev": abs(st.norm_squared() - 1.0)}
+    legs["clocks"] = clocks2.stop()
     check = qft33_check(st, step, ops)
     del st, nat
 
@@ -464,6 +493,7 @@ def run_single(args) -> None:
                    "reference_fuser_ops": len(ref_ops),
                    "reference_fuser_gates_per_s": len(gates) / (ref_ms / 1000.0),
                    "fold_k6_gates_per_s": len(gates) / (k6_ms / 1000.0),
+                   "fp32_level_tc_gates_per_s": len(gates) / (tc_ms / 1000.0),
                    "l2": "state 64 GiB >> 126 MB L2 (no flush needed)", "parallelism": "single segment",
                    "vs_baseline_ref": "qsim-mgpu 1xH100 QFT-33 k=5: 577 gates/1.21 s (PAPER.md:285-288)"},
         "fused_ops_per_s": len(ops) / (ms_step / 1000.0),
@@ -477,6 +507,7 @@ def run_single(args) -> None:
         "clocks": clk,
         "kernels": kernels,
         "check": check,
+        "legs": legs,
     }
     print(json.dumps(line), flush=True)
 

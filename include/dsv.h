@@ -55,6 +55,11 @@ typedef struct dsv_state dsv_state;
 const char* dsv_last_error(void);
 int dsv_version(void);
 int dsv_device_count(int* out);
+/* Kernel-selection switches, otherwise read once from the environment:
+ * "tc" (DSV_TC: tensor-core windows), "tc8" (DSV_TC8: int8-digit tcgen05
+ * kernels; 0 selects the bf16-limb fp32-level tc.cu / tc6.cu), "low", "lowt",
+ * "dblk8", "blk8", "wt".  Process-wide; takes effect for the next call. */
+int dsv_config_set(const char* key, int value);
 /* total number of this library's kernel launches so far (all states) */
 int dsv_launch_count(uint64_t* out);
 

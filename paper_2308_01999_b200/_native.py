@@ -41,6 +41,7 @@ SIGNATURES: dict[str, list] = {
     "dsv_version": [],
     "dsv_device_count": [C.POINTER(_int)],
     "dsv_launch_count": [_u64p],
+    "dsv_config_set": [C.c_char_p, _int],
     "dsv_state_create": [_int, _int, _int, C.POINTER(_vp)],
     "dsv_pool_release": [_int],
     "dsv_state_destroy": [_vp],
@@ -107,7 +108,10 @@ def lib():
                 "(python -c 'import __graft_entry__ as g; g.build()')"
             )
         handle = C.CDLL(str(path), mode=C.RTLD_GLOBAL)
+        ab_build = "DSV_LIBRARY" in os.environ  # an older build for same-box A/B runs may lack newer entries
         for name, argtypes in SIGNATURES.items():
+            if ab_build and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPES.get(name, C.c_int)
@@ -185,6 +189,11 @@ def device_count() -> int:
 def pool_release(device: int = -1) -> None:
     """Free the cached state buffers (device < 0: every device)."""
     call("dsv_pool_release", int(device))
+
+
+def config_set(key: str, value: int) -> None:
+    """Kernel-selection switch (include/dsv.h dsv_config_set)."""
+    call("dsv_config_set", key.encode(), int(value))
 
 
 def launch_count() -> int:

@@ -40,45 +40,52 @@ const bool g_disable_tile = [] {
 
 // Tensor-core path for k = 4, 5 complex64 dense / phased windows (tc.cu).
 // DSV_TC=0 disables it (A/B runs against the CUDA-core kernels).
-const bool g_tc_env = [] {
+bool g_tc_env = [] {
   const char* e = std::getenv("DSV_TC");
   return !(e && e[0] == '0');
 }();
 
 // 8-bit integer-digit tensor-core kernel for k = 4, 5 (tc8.cu); DSV_TC8=0 selects
 // the bf16-limb kernel (tc.cu) instead.
-const bool g_tc8_env = [] {
+bool g_tc8_env = [] {
   const char* e = std::getenv("DSV_TC8");
+  return !(e && e[0] == '0');
+}();
+
+// Warp-specialised pipeline for the int8-digit kernel (tc8.cu k_dense_tc8ws);
+// DSV_TC8WS=0 selects the two-group kernel.
+bool g_tc8ws_env = [] {
+  const char* e = std::getenv("DSV_TC8WS");
   return !(e && e[0] == '0');
 }();
 
 // Lane-split kernel for k <= 3 complex64 windows on the lowest k bits (low.cu).
 // DSV_LOW=0 disables it.
-const bool g_low_env = [] {
+bool g_low_env = [] {
   const char* e = std::getenv("DSV_LOW");
   return !(e && e[0] == '0');
 }();
 
 // Warp-transposed phased k = 3 low-window kernel (low.cu k_dense_lowt); DSV_LOWT=0 disables.
-const bool g_lowt_env = [] {
+bool g_lowt_env = [] {
   const char* e = std::getenv("DSV_LOWT");
   return !(e && e[0] == '0');
 }();
 
 // 64-byte-block kernel for complex64 dense gates inside bits 0..2 (perm.cu); DSV_DBLK8=0 disables.
-const bool g_dblk8_env = [] {
+bool g_dblk8_env = [] {
   const char* e = std::getenv("DSV_DBLK8");
   return !(e && e[0] == '0');
 }();
 
 // 64-byte-block kernel for complex64 permutations inside bits 0..2 (perm.cu); DSV_BLK8=0 disables.
-const bool g_blk8_env = [] {
+bool g_blk8_env = [] {
   const char* e = std::getenv("DSV_BLK8");
   return !(e && e[0] == '0');
 }();
 
 // Warp-transpose kernel for dense gates inside the lowest 6 bits (wt.cu); DSV_WT=0 disables.
-const bool g_wt_env = [] {
+bool g_wt_env = [] {
   const char* e = std::getenv("DSV_WT");
   return !(e && e[0] == '0');
 }();
@@ -485,6 +492,14 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
       ++e_b;  // the rounded maximum reached the digit range: one more bit of headroom
     }
     d.e_b = e_b;
+    // warp-specialised pipeline only where it measured faster on the same box
+    // (tools/_patt2.py, tools/_ab_qft.py at n = 33): plain windows with index
+    // bit 0 the lowest target, whose member pairs move as 16-byte units
+    // (0.87-0.89 -> 0.97 of the copy peak).  Elsewhere it is a wash or up to
+    // 4 % slower (contiguous and phased windows, most scattered-target QV
+    // windows): DSV_TC8WS=0 disables it, and the kernel stays available for
+    // A/B through dsv_config_set("tc8ws", ...).
+    d.ws = (g_tc8ws_env && terms.empty() && d.mode == 3) ? 1 : 0;
     std::vector<unsigned char> host8(size_t(3) * KK * 128, 0);
     for (int n = 0; n < KK; ++n)
       for (int kk = 0; kk < KK; ++kk) {
@@ -706,6 +721,23 @@ void minus_i_pow(int ny, double* re, double* im) {
 }  // namespace
 
 extern "C" {
+
+int dsv_config_set(const char* key, int value) {
+  // the kernel-selection switches otherwise read once from the environment
+  // (DSV_TC, DSV_TC8, DSV_LOW, DSV_LOWT, DSV_DBLK8, DSV_BLK8, DSV_WT)
+  static const struct {
+    const char* name;
+    bool* flag;
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
+               {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
+  if (!key) return fail(DSV_EINVAL, "null key");
+  for (const auto& k : kKeys)
+    if (std::strcmp(k.name, key) == 0) {
+      *k.flag = value != 0;
+      return DSV_OK;
+    }
+  return fail(DSV_EINVAL, "unknown config key '%s'", key);
+}
 
 const char* dsv_last_error(void) { return g_err.c_str(); }
 int dsv_version(void) { return 1; }

@@ -52,6 +52,7 @@ struct TcDesc {
   int nib_shift[16];
   uint64_t offs[64];
   int tshift;  // targets are bits tshift .. tshift + k - 1 (member j at offset j << tshift), else -1
+  int ws;      // tc8: warp-specialised pipeline (loader / converter+MMA / epilogue warps), else the 2-group kernel
 };
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);

@@ -495,6 +495,442 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
   }
 }
 
+// ---- warp-specialised pipeline ---------------------------------------------------------
+// The same arithmetic as k_dense_tc8, with the per-tile work split over three
+// warp roles that run concurrently on different tiles (14 warps per SM instead
+// of 8; a role never waits on another role's instruction latency):
+//   warps 0-1  loaders: cp.async two rows each of the tile into a ring stage,
+//              arrive on full[stage] when the copies land; phased windows
+//              also compute the tile's phase data into the stage;
+//   warps 2-5  converters (thread = row, TMEM lane quarter = warp % 4): read
+//              the row, apply the phase, scale and split into int8 digits,
+//              tcgen05.st them into TMEM slot (i & 1), free the stage; one
+//              thread issues the 3 x KSTEPS MMAs and commits;
+//   warps 6-13 epilogue (two warps per lane quarter, one per half of the
+//              output columns): wait for the MMAs, tcgen05.ld the three
+//              accumulators, combine, store to HBM, reset the accumulators
+//              to the magic start value and hand the TMEM slot back.
+// mbarriers: full[s] (64 cp.async arrivals + 64 loader arrivals), empty[s]
+// (128 converters), slot_free[t] (256 epilogue threads; completion 0 = the
+// initial accumulator fill), acc_full[t] (MMA commit), meta_full[t] (the
+// converters' per-row scale / offset for the epilogue).  The epilogue has the
+// most dependent work per tile (ncu: converters waited on slot_free and
+// loaders on empty with one epilogue warp per quarter), hence two per quarter.
+template <int K, bool PHASED>
+struct Tc8WsLayout {
+  static constexpr int D = 1 << K;
+  static constexpr int N0 = 2 * D;
+  static constexpr int B_BYTES = 3 * N0 * 128;
+  static constexpr int BAR = B_BYTES;              // barriers + TMEM slot + magic words (256 B)
+  static constexpr int META = BAR + 256;           // [2 slots][128 rows] float2 (scale, cm)
+  static constexpr int PST = META + 2 * 128 * 8;   // per-stage phase data
+  static constexpr int PSTAGE = PHASED ? (32 + D * 8) : 0;  // tile-uniform angle sums [8] + phase vector [D]
+  static constexpr int STAGE = 128 * D * 8;
+  static constexpr int SMEM_MAX = 227 * 1024 - 1024;
+  static constexpr int NS_FIT = (SMEM_MAX - PST - 1024) / (STAGE + PSTAGE);
+  static constexpr int NSTAGE = NS_FIT > 8 ? 8 : NS_FIT;
+  static constexpr int RING = ((PST + NSTAGE * PSTAGE + 1023) / 1024) * 1024;
+  static constexpr int BYTES = RING + NSTAGE * STAGE;
+  static_assert(NSTAGE >= 3, "ring must hold three tiles");
+  static_assert(BYTES <= SMEM_MAX, "shared memory plan");
+};
+
+template <int K, bool PHASED, int MODE>
+__global__ void __launch_bounds__(448, 1)
+k_dense_tc8ws(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, const float4* __restrict__ tab,
+              float2* __restrict__ sv) {
+  using L = Tc8WsLayout<K, PHASED>;
+  using LM = Tc8Layout<K>;  // TMEM plan and MMA shapes
+  constexpr bool PAIR = MODE == kTcPair;
+  constexpr bool LOWT = MODE == kTcLow;
+  constexpr bool ROW2 = MODE == kTcRow2;
+  constexpr int D = L::D;
+  constexpr int N0 = L::N0;
+  constexpr int S = L::NSTAGE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t raw_base = smem_u32(smem_raw);
+  const uint32_t sbase = (raw_base + 1023u) & ~1023u;
+  unsigned char* sm = smem_raw + (sbase - raw_base);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int role = warp < 2 ? 0 : (warp < 6 ? 1 : 2);
+  // converters / epilogue: the row is this thread's TMEM lane (quarter = warp % 4)
+  const int row = role == 0 ? tid : (((warp & 3) << 5) | (tid & 31));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 192);
+  auto FULL = [&](int s) { return sbase + L::BAR + 8 * s; };
+  auto EMPTY = [&](int s) { return sbase + L::BAR + 64 + 8 * s; };
+  auto SLOTFREE = [&](int t) { return sbase + L::BAR + 128 + 8 * t; };
+  auto ACCFULL = [&](int t) { return sbase + L::BAR + 144 + 8 * t; };
+  auto METAFULL = [&](int t) { return sbase + L::BAR + 160 + 8 * t; };
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid < 2) reinterpret_cast<uint32_t*>(sm + L::BAR + 200)[tid] = kAccInit;
+  if (tid == 32) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(FULL(s), 128);
+      mbar_init(EMPTY(s), 128);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(SLOTFREE(t), 256);
+      mbar_init(ACCFULL(t), 1);
+      mbar_init(METAFULL(t), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 3 * N0 * 8; i += 448) {
+    const int r = i / 8, c16 = i % 8;
+    *reinterpret_cast<uint4*>(sm + r * 128 + ((c16 ^ (r & 7)) << 4)) = bmat[i];
+  }
+  const uint64_t step = gridDim.x;
+  auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + uint64_t(i) * step; };
+  const uint64_t e0 = expand(p.g, 0);
+  const uint64_t rowoff = expand(p.g, row) ^ e0;
+  float2* meta = reinterpret_cast<float2*>(sm + L::META);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (*tmem_slot != 0u) __trap();  // whole-TMEM allocation starts at lane 0, column 0
+  const uint32_t tq = uint32_t((warp & 3) * 32) << 16;
+
+  if (role == 0) {
+    // ===== loaders =====
+#pragma unroll 1
+    for (int i = 0;; ++i) {
+      const uint64_t tl = tile_of(i);
+      if (tl >= p.ntiles) break;
+      const int s = i % S;
+      if (i >= S) mbar_wait(EMPTY(s), uint32_t((i / S) - 1) & 1u);
+      const uint64_t tb = expand(p.g, tl * 128);
+      const uint32_t st0 = sbase + L::RING + s * L::STAGE;
+#pragma unroll 1
+      for (int rr = 0; rr < 2; ++rr) {
+      const int row = tid + 64 * rr;  // this loader's two rows
+      const uint64_t rowoff = expand(p.g, row) ^ e0;
+      const int prow = 2 * (row & 63);
+      const int jpar = row >> 6;
+      const uint64_t prowoff = expand(p.g, prow) ^ e0;
+      if constexpr (LOWT) {
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) {
+          const int q = row + 128 * m;
+          const int r = q / (D / 2), c = q % (D / 2);
+          cp_async16(st0 + r * (D * 8) + ((c ^ (r & 7)) << 4), sv + tb + 2 * q);
+        }
+      } else if constexpr (ROW2) {
+        const uint64_t b = tb | rowoff;
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) cp_async16(st0 + m * 2048 + row * 16, sv + b + p.offs[2 * m]);
+      } else if constexpr (PAIR) {
+        const uint64_t b = tb | prowoff;
+        if (p.tshift >= 0) {
+          const float2* src = sv + b + (uint64_t(jpar) << p.tshift);
+          const uint64_t stride = uint64_t(2) << p.tshift;
+#pragma unroll
+          for (int jj = 0; jj < D / 2; ++jj) cp_async16(st0 + prow * 8 + (2 * jj + jpar) * 1024, src + jj * stride);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < D / 2; ++jj) {
+            const uint64_t o = jpar ? p.offs[2 * jj + 1] : p.offs[2 * jj];
+            cp_async16(st0 + prow * 8 + (2 * jj + jpar) * 1024, sv + b + o);
+          }
+        }
+      } else {
+        const uint64_t b = tb | rowoff;
+        if (p.tshift >= 0) {
+          const float2* src = sv + b;
+          const uint64_t stride = uint64_t(1) << p.tshift;
+#pragma unroll
+          for (int j = 0; j < D; ++j) cp_async8(st0 + row * 8 + j * 1024, src + j * stride);
+        } else {
+#pragma unroll
+          for (int j = 0; j < D; ++j) cp_async8(st0 + row * 8 + j * 1024, sv + b + p.offs[j]);
+        }
+      }
+      }
+      cp_async_mbar_arrive(FULL(s));
+      if constexpr (PHASED) {
+        // tile-uniform angle sums (constant bank, the same for every thread);
+        // row-varying nibbles are added by the converters (rows' own part)
+        unsigned char* ps = sm + L::PST + s * L::PSTAGE;
+        float a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = 0.f;
+#pragma unroll
+        for (int c = 0; c < kTcMaxNib; ++c) {
+          if (c >= p.nnib_row && c < p.nnib) {
+            const int r = (c * 16 + int((tb >> p.nib_shift[c]) & 15u)) * 2;
+            const float4 x = p.ctab[r], y = p.ctab[r + 1];
+            a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w;
+            a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
+          }
+        }
+        if (p.coop) {  // one phase vector per tile: member j = tid - (64 - D)
+          const int j = tid - (64 - D);
+          if (j >= 0) {
+            float ang = a[K];
+#pragma unroll
+            for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
+            float sn, cs;
+            sincos_unit(ang, &sn, &cs);
+            reinterpret_cast<float2*>(ps + 32)[j] = make_float2(cs, sn);
+          }
+        } else if (tid == 0) {
+          float4* au = reinterpret_cast<float4*>(ps);
+          au[0] = make_float4(a[0], a[1], a[2], a[3]);
+          au[1] = make_float4(a[4], a[5], a[6], a[7]);
+        }
+      }
+      mbar_arrive(FULL(s));
+    }
+    cp_async_wait<0>();
+  } else if (role == 1) {
+    // ===== converters + MMA issue =====
+    // row-varying phase nibbles (non-coop windows): this row's angle sums from
+    // the global table, loaded one tile ahead so the latency is off the path
+    float ra[8];
+    auto row_part = [&](uint64_t tl) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ra[q] = 0.f;
+      if (tl >= p.ntiles) return;
+      const uint64_t b = expand(p.g, tl * 128) | rowoff;
+#pragma unroll
+      for (int c = 0; c < kTcMaxNib; ++c) {
+        if (c < p.nnib_row) {
+          const int r = (c * 16 + int((b >> p.nib_shift[c]) & 15u)) * 2;
+          const float4 x = __ldg(tab + r), y = __ldg(tab + r + 1);
+          ra[0] += x.x; ra[1] += x.y; ra[2] += x.z; ra[3] += x.w;
+          ra[4] += y.x; ra[5] += y.y; ra[6] += y.z; ra[7] += y.w;
+        }
+      }
+    };
+    if (PHASED && !p.coop) row_part(tile_of(0));
+#pragma unroll 1
+    for (int i = 0;; ++i) {
+      const uint64_t tl = tile_of(i);
+      if (tl >= p.ntiles) break;
+      const int s = i % S;
+      const int t = i & 1;
+      mbar_wait(FULL(s), uint32_t(i / S) & 1u);
+      const unsigned char* stg = sm + L::RING + s * L::STAGE;
+      float2 v[D];
+      if constexpr (ROW2) {
+#pragma unroll
+        for (int m = 0; m < D / 2; ++m) {
+          const float4 x = *reinterpret_cast<const float4*>(stg + m * 2048 + row * 16);
+          v[2 * m] = make_float2(x.x, x.y);
+          v[2 * m + 1] = make_float2(x.z, x.w);
+        }
+      } else if constexpr (LOWT) {
+#pragma unroll
+        for (int c = 0; c < D / 2; ++c) {
+          const float4 x = *reinterpret_cast<const float4*>(stg + row * (D * 8) + ((c ^ (row & 7)) << 4));
+          v[2 * c] = make_float2(x.x, x.y);
+          v[2 * c + 1] = make_float2(x.z, x.w);
+        }
+      } else {
+        const float2* raw = reinterpret_cast<const float2*>(stg) + row;
+#pragma unroll
+        for (int j = 0; j < D; ++j) v[j] = raw[j * 128];
+      }
+      if constexpr (PHASED) {
+        const unsigned char* ps = sm + L::PST + s * L::PSTAGE;
+        if (p.coop) {
+          const float2* P = reinterpret_cast<const float2*>(ps + 32);
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const float2 x = v[j], f = P[j];
+            v[j] = make_float2(x.x * f.x - x.y * f.y, x.x * f.y + x.y * f.x);
+          }
+        } else {
+          const float4* au = reinterpret_cast<const float4*>(ps);
+          const float4 h0 = au[0], h1 = au[1];
+          const float a[8] = {h0.x + ra[0], h0.y + ra[1], h0.z + ra[2], h0.w + ra[3],
+                              h1.x + ra[4], h1.y + ra[5], h1.z + ra[6], h1.w + ra[7]};
+          row_part(tile_of(i + 1));  // next tile's row part (loads in flight during this tile)
+          float2 P[D];
+          sincos_red(a[K], &P[0].y, &P[0].x);
+#pragma unroll
+          for (int m = 0; m < K; ++m) {
+            float es, ec;
+            sincos_red(a[m], &es, &ec);
+#pragma unroll
+            for (int j = 0; j < (1 << m); ++j) {
+              const float2 q = P[j];
+              P[j + (1 << m)] = make_float2(q.x * ec - q.y * es, q.x * es + q.y * ec);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const float2 x = v[j];
+            v[j] = make_float2(x.x * P[j].x - x.y * P[j].y, x.x * P[j].y + x.y * P[j].x);
+          }
+        }
+      }
+      mbar_arrive(EMPTY(s));  // the row (and its phase data) is in registers: stage free
+      float mx = 0.f;
+#pragma unroll
+      for (int j = 0; j < D; ++j) mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
+      const int e_row = min(max(int((__float_as_uint(mx) >> 23) & 0xFF) - 126, p.emin), p.emax);
+      const float sc_in = pow2f(22 - e_row);
+      // slot t: the epilogue has drained tile i - 2 (completion 0 = initial fill)
+      mbar_wait(SLOTFREE(t), uint32_t(i >> 1) & 1u);
+      fence_after();
+      meta[t * 128 + row] = make_float2(pow2f(e_row + p.e_b - 29), -197379.f * pow2f(e_row + p.e_b - 7));
+      const uint32_t tl0 = uint32_t(t * 256) + tq;
+      // digits -> TMEM in blocks of 8 columns (column c: K = 4c..4c+3 = (re, im) of members 2c, 2c+1)
+#pragma unroll
+      for (int cb = 0; cb < N0 / 4; cb += 8) {
+        uint32_t la2[8], la1[8], la0[8];
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const int c = cb + cc;
+          const uint32_t w0 = __float_as_uint(__fmaf_rn(v[2 * c].x, sc_in, kMagic)) + kDigitOff;
+          const uint32_t w1 = __float_as_uint(__fmaf_rn(v[2 * c].y, sc_in, kMagic)) + kDigitOff;
+          const uint32_t w2 = __float_as_uint(__fmaf_rn(v[2 * c + 1].x, sc_in, kMagic)) + kDigitOff;
+          const uint32_t w3 = __float_as_uint(__fmaf_rn(v[2 * c + 1].y, sc_in, kMagic)) + kDigitOff;
+          const uint32_t p01 = __byte_perm(w0, w1, 0x5140), p23 = __byte_perm(w2, w3, 0x5140);
+          la0[cc] = __byte_perm(p01, p23, 0x5410) ^ 0x80808080u;
+          la1[cc] = __byte_perm(p01, p23, 0x7632) ^ 0x80808080u;
+          la2[cc] = __byte_perm(__byte_perm(w0, w1, 0x0062), __byte_perm(w2, w3, 0x0062), 0x5410);
+        }
+        tmem_st8(tl0 + uint32_t(LM::T_A2 + cb), la2);
+        tmem_st8(tl0 + uint32_t(LM::T_A1 + cb), la1);
+        tmem_st8(tl0 + uint32_t(LM::T_A0 + cb), la0);
+      }
+      mbar_arrive(METAFULL(t));
+      tmem_wait_st();
+      fence_before();
+      named_sync(1, 128);
+      if (row == 0) {
+        fence_after();
+        if (t == 0) issue_mma8<K, 0>(sbase);
+        else issue_mma8<K, 1>(sbase);
+        mma_commit(ACCFULL(t));
+      }
+    }
+  } else {
+    // ===== epilogue =====
+    uint32_t mg[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mg[q] = reinterpret_cast<const uint32_t*>(sm + L::BAR + 200)[q & 1];
+    // this warp's half of the output columns (k = 4: one half of 32 columns
+    // per accumulator, the second warp of the quarter only resets)
+    constexpr int NH = N0 / 32 > 0 ? N0 / 32 : 1;
+    const int half = (warp - 6) >> 2;
+    auto reset = [&](uint32_t tlane) {
+      if constexpr (NH == 1) {  // k = 4: the first warp of the quarter owns all 32 columns
+        if (half == 0)
+#pragma unroll
+          for (int q = 0; q < 3 * N0 / 8; ++q) tmem_st8(tlane + uint32_t(LM::T_HI + 8 * q), mg);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int q = 0; q < N0 / 16; ++q)
+            tmem_st8(tlane + uint32_t(LM::T_HI + a * N0 + half * (N0 / 2) + 8 * q), mg);
+      }
+    };
+    // accumulators of both slots start at the magic value: completion 0 of slot_free
+    reset(tq);
+    reset(uint32_t(256) + tq);
+    tmem_wait_st();
+    fence_before();
+    mbar_arrive(SLOTFREE(0));
+    mbar_arrive(SLOTFREE(1));
+    // out = scale (acc_h 2^16 + acc_m 2^8 + acc_l): the accumulators read
+    // back as M + acc, so with cm = -65793 M scale three fmas do it, hi first
+    // (acc_h 2^16 - 257 M is exact; the two later sums round once each)
+    auto combine = [](float h, float m, float l, float scale, float s8, float s16, float cm) {
+      return __fmaf_rn(l, scale, __fmaf_rn(m, s8, __fmaf_rn(h, s16, cm)));
+    };
+#pragma unroll 1
+    for (int i = 0;; ++i) {
+      const uint64_t tl = tile_of(i);
+      if (tl >= p.ntiles) break;
+      const int t = i & 1;
+      const uint64_t b = expand(p.g, tl * 128) | rowoff;
+      mbar_wait(ACCFULL(t), uint32_t(i >> 1) & 1u);
+      mbar_wait(METAFULL(t), uint32_t(i >> 1) & 1u);
+      fence_after();
+      const float2 mt = meta[t * 128 + row];
+      const float scale = mt.x, cm = mt.y;
+      const float s8 = scale * 256.f, s16 = scale * 65536.f;
+      const uint32_t tlane = uint32_t(t * 256) + tq;
+#pragma unroll
+      for (int hh = 0; hh < (NH + 1) / 2; ++hh) {
+        const int h = NH == 1 ? 0 : half;
+        if (NH == 1 && half == 1) break;
+        float ch[32], cmid[32], cl[32];
+        tmem_ld32(tlane + uint32_t(LM::T_HI + h * 32), ch);
+        tmem_ld32(tlane + uint32_t(LM::T_MID + h * 32), cmid);
+        tmem_ld32(tlane + uint32_t(LM::T_LO + h * 32), cl);
+        auto val = [&](int c) { return combine(ch[c], cmid[c], cl[c], scale, s8, s16, cm); };
+        if constexpr (LOWT) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            stcs32(sv + b + h * 16 + 4 * q, val(8 * q), val(8 * q + 1), val(8 * q + 2), val(8 * q + 3),
+                   val(8 * q + 4), val(8 * q + 5), val(8 * q + 6), val(8 * q + 7));
+        } else if constexpr (ROW2) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcs(reinterpret_cast<float4*>(sv + b + p.offs[h * 16 + 2 * q]),
+                   make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3)));
+        } else if constexpr (PAIR && !PHASED) {
+          const bool odd = row & 1;
+          const uint64_t be = b - (odd ? 1 : 0);
+          float2* dst = sv + be + (p.tshift >= 0 ? (uint64_t(h * 16 + (odd ? 1 : 0)) << p.tshift) : 0);
+          const uint64_t stride = p.tshift >= 0 ? (uint64_t(2) << p.tshift) : 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float o[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) o[c] = val(4 * q + c);
+            const float sx = odd ? o[0] : o[2], sy = odd ? o[1] : o[3];
+            const float rx = __shfl_xor_sync(0xffffffffu, sx, 1), ry = __shfl_xor_sync(0xffffffffu, sy, 1);
+            const float4 w = odd ? make_float4(rx, ry, o[2], o[3]) : make_float4(o[0], o[1], rx, ry);
+            if (p.tshift >= 0) {
+              __stcs(reinterpret_cast<float4*>(dst + q * stride), w);
+            } else {
+              const uint64_t oj = odd ? p.offs[h * 16 + 2 * q + 1] : p.offs[h * 16 + 2 * q];
+              __stcs(reinterpret_cast<float4*>(sv + be + oj), w);
+            }
+          }
+        } else {
+          if (p.tshift >= 0) {
+            float2* dst = sv + b + (uint64_t(h * 16) << p.tshift);
+            const uint64_t stride = uint64_t(1) << p.tshift;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              __stcs(dst, make_float2(val(2 * q), val(2 * q + 1)));
+              dst += stride;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) __stcs(sv + b + p.offs[h * 16 + q], make_float2(val(2 * q), val(2 * q + 1)));
+          }
+        }
+      }
+      // accumulators back to the magic start value, slot handed back
+      reset(tlane);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(SLOTFREE(t));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512) : "memory");
+  }
+}
+
 template <int K, bool PHASED, int MODE>
 static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
   using L = Tc8Layout<K>;
@@ -518,10 +954,28 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
   for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
   if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));
-  const int smem = L::BYTES + 1024;
-  static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
+  if (d.ws) {
+    using LW = Tc8WsLayout<K, PHASED>;
+    const int smem = LW::BYTES + 1024;
+    static bool attr_ws[64] = {false};
+    if (dev >= 0 && dev < 64 && !attr_ws[dev]) {
+      cudaError_t e =
+          cudaFuncSetAttribute(k_dense_tc8ws<K, PHASED, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr_ws[dev] = true;
+    }
+    uint64_t blocks = uint64_t(device_sm_count());
+    if (blocks > p.ntiles) blocks = p.ntiles;
+    if (blocks == 0) return cudaSuccess;
+    k_dense_tc8ws<K, PHASED, MODE><<<unsigned(blocks), 448, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+                                                                      static_cast<const float4*>(d_tab),
+                                                                      static_cast<float2*>(sv));
+    return cudaGetLastError();
+  }
+  const int smem = L::BYTES + 1024;
+  static bool attr_set[64] = {false};
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(k_dense_tc8<K, PHASED, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

@@ -398,3 +398,40 @@ def test_wt_low_targets_vs_oracle(dtype):
             assert prof.get("dense_wt", {}).get("count", 0) == 1, prof
         tol = 2e-6 if dtype == np.complex64 else 1e-13
         assert _rel_err(sv.amplitudes, want) <= tol, (targets, prof, _rel_err(sv.amplitudes, want))
+
+
+@pytest.mark.parametrize("targets", [(5, 6, 7, 8, 9), (2, 9, 15, 3, 12), (1, 4, 6, 9, 12), (0, 5, 9, 12, 14),
+                                     (0, 1, 2, 3, 4), (0, 1, 2, 3), (0, 2, 5, 7)])
+def test_tc8_warp_specialised_kernel_all_layouts(targets):
+    """The warp-specialised int8-digit kernel (tc8.cu k_dense_tc8ws: loader /
+    converter / epilogue warps) forced on for every copy mode, plain and
+    phased, against the oracle and the two-group kernel."""
+    from paper_2308_01999_b200.fusion_fold import PhasedDenseGate
+
+    rng = np.random.default_rng(sum(targets) + 31 * len(targets))
+    n = 16
+    k = len(targets)
+    m = G.random_unitary(1 << k, rng)
+    others = [q for q in range(n) if q not in targets]
+    cross = tuple((int(targets[i]), int(others[(3 * i) % len(others)]), float(rng.uniform(0, 6))) for i in range(k))
+    outside = ((int(others[-1]), 0.7),)
+    st = random_state(n, rng, np.complex64)
+    for op in (G.DenseGate(m, tuple(targets)), PhasedDenseGate(m, tuple(targets), cross, outside)):
+        want = st.astype(np.complex128)
+        if isinstance(op, PhasedDenseGate):
+            ang = _phase_angles(n, list(range(n)), [(q, b, t) for q, b, t in cross], list(outside))
+            want = want * np.exp(1j * ang)
+        O.apply_dense(want, n, m, list(targets))
+        outs = []
+        for ws in (1, 0):
+            N.config_set("tc8ws", ws)
+            try:
+                sv = StateVector.from_amplitudes(st)
+                nat = _tc_launches(sv)
+                sv.apply(op)
+                assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1
+                outs.append(sv.amplitudes)
+            finally:
+                N.config_set("tc8ws", 1)
+        for o in outs:
+            assert _rel_err(o, want) <= 2 * REL
