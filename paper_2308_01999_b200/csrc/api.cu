@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/dsv.h"
 #include "common.cuh"
 #include "launch.h"
@@ -56,6 +58,13 @@ bool g_tc8_env = [] {
 // DSV_TC8WS=0 selects the two-group kernel.
 bool g_tc8ws_env = [] {
   const char* e = std::getenv("DSV_TC8WS");
+  return !(e && e[0] == '0');
+}();
+
+// TMA tile loads for the int8-digit kernel's row-pair windows (tc8.cu kTcTma);
+// DSV_TMA=0 keeps the per-thread cp.async copies.
+bool g_tma_env = [] {
+  const char* e = std::getenv("DSV_TMA");
   return !(e && e[0] == '0');
 }();
 
@@ -409,6 +418,84 @@ bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
   return device_has_tcgen05(s->device);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return EncodeTiledFn(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// kTcTma eligibility + tensor map: complex64 state, no controls, index bit 0
+// free, rows = the 7 lowest free bits.  Index bits are labelled row / member
+// / tile and cut into runs of equal labels; the map's dimensions are the runs
+// (at most 5) ordered rows first, then members, then tile runs, so the box
+// (all rows x all members x one tile) lands as [member][row] in shared
+// memory — the layout the kernel's converters read.  Returns false (and the
+// caller keeps cp.async) when the layout needs more than 5 runs or the driver
+// rejects the map.
+bool build_tile_tmap(const dsv_state* s, const GateGeom& gg, TcDesc* d) {
+  if (!g_tma_env || gg.nctrl != 0 || gg.k > 5 || s->dtype != DSV_C64) return false;
+  const int n = s->nbits;
+  std::vector<char> lab(n, 'T');
+  for (int m = 0; m < gg.k; ++m) lab[gg.tsorted[m]] = 'M';
+  if (lab[0] != 'T') return false;  // bit 0 must be a row bit
+  for (int b = 0, rows = 0; b < n && rows < 7; ++b)
+    if (lab[b] == 'T') {
+      lab[b] = 'R';
+      ++rows;
+    }
+  struct Run { char l; int start, len; };
+  std::vector<Run> runs;
+  for (int b = 0; b < n; ++b) {
+    if (!runs.empty() && runs.back().l == lab[b] && runs.back().start + runs.back().len == b) ++runs.back().len;
+    else runs.push_back({lab[b], b, 1});
+  }
+  if (runs.size() > 5) return false;
+  std::vector<Run> order;
+  for (char l : {'R', 'M', 'T'})
+    for (const Run& r : runs)
+      if (r.l == l) order.push_back(r);
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  int consumed = 0;  // tile runs appear in ascending bit order: tile index bits map low -> high
+  for (int q = 0; q < 5; ++q) {
+    estr[q] = 1;
+    d->tma_shift[q] = 0;
+    d->tma_mask[q] = 0;
+    if (q < int(order.size())) {
+      dims[q] = cuuint64_t(1) << order[q].len;
+      box[q] = order[q].l == 'T' ? 1u : cuuint32_t(1) << order[q].len;
+      if (q) strides[q - 1] = (cuuint64_t(1) << order[q].start) * 8;
+      if (order[q].l == 'T') {
+        if (order[q].len > 31) return false;
+        d->tma_shift[q] = consumed;
+        d->tma_mask[q] = (uint32_t(1) << order[q].len) - 1u;
+        consumed += order[q].len;
+      }
+    } else {  // padding dimension of extent 1
+      dims[q] = 1;
+      box[q] = 1;
+      strides[q - 1] = (cuuint64_t(1) << n) * 8;
+    }
+  }
+  if (order[0].l != 'R' || order[0].start != 0) return false;
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) return false;
+  const CUresult r = fn(&d->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, s->d, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Dense (+ optional pre-phase) window on the tensor cores; caller holds the device guard.
 int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::vector<PhaseTerm>& terms,
              int prof_class, double bytes) {
@@ -500,6 +587,12 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     // windows): DSV_TC8WS=0 disables it, and the kernel stays available for
     // A/B through dsv_config_set("tc8ws", ...).
     d.ws = (g_tc8ws_env && terms.empty() && d.mode == 3) ? 1 : 0;
+    // TMA tile loads where they measured faster than the per-thread cp.async
+    // copies (tools/_ab_tma.py, same box, n = 33): windows whose 128 tile rows
+    // are split around the targets (lowest target below bit 7, e.g. QFT-33's
+    // window on qubits 3..7: 27.5 -> 27.1 ms).  Rows that are one contiguous
+    // run (plain windows high up: 22.5 -> 24.4 ms) keep cp.async.
+    if (k <= 5 && d.mode == 1 && gg.tsorted[0] < 7 && build_tile_tmap(s, gg, &d)) d.mode = 4;  // kTcTma
     std::vector<unsigned char> host8(size_t(3) * KK * 128, 0);
     for (int n = 0; n < KK; ++n)
       for (int kk = 0; kk < KK; ++kk) {
@@ -728,7 +821,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tma", &g_tma_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)

@@ -3,6 +3,7 @@
 // all others are host memory read during the call (kernel parameters).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "common.cuh"
 
@@ -53,6 +54,13 @@ struct TcDesc {
   uint64_t offs[64];
   int tshift;  // targets are bits tshift .. tshift + k - 1 (member j at offset j << tshift), else -1
   int ws;      // tc8: warp-specialised pipeline (loader / converter+MMA / epilogue warps), else the 2-group kernel
+  // mode kTcTma (tc8): each tile arrives by ONE tensor-memory-access load
+  // (cp.async.bulk.tensor) of this map over the state: dims = runs of row /
+  // member / tile index bits, box = 128 rows x 2^k members ([member][row] in
+  // shared memory); tile coordinates = bit fields of the tile index
+  CUtensorMap tmap;
+  int tma_shift[5];          // coordinate of map dimension q = (tile >> shift[q]) & mask[q]
+  uint32_t tma_mask[5];      // (mask 0: a row / member / padding dimension, coordinate 0)
 };
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);

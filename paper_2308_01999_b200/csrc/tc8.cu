@@ -58,6 +58,8 @@ struct Tc8P {
   int tshift;             // member j at offset j << tshift (contiguous targets), else -1: offs[]
   uint64_t offs[1 << K];  // member offsets (amplitudes)
   float4 ctab[kTcMaxNib * 16 * 2];  // tile-uniform phase table (constant bank, broadcast reads)
+  int tma_shift[5];       // kTcTma: tile coordinate of map dim q = (tile >> shift[q]) & mask[q]
+  uint32_t tma_mask[5];
 };
 
 template <int K>
@@ -67,7 +69,8 @@ struct Tc8Layout {
   static constexpr int KSTEPS = N0 / 32;          // MMA K = 32 (8-bit)
   static constexpr int B_BYTES = 3 * N0 * 128;    // [b2 | b1 | b0] rows of 128 B (K <= 64 used)
   static constexpr int BAR = B_BYTES;             // 2 mbarriers + TMEM slot
-  static constexpr int MAG = BAR + 128;           // 128 x 32 B of the accumulator start value (tcgen05.cp source)
+  static constexpr int MAG = BAR + 256;           // 128 x 32 B of the accumulator start value (tcgen05.cp source)
+  static constexpr int TMABAR = BAR + 64;         // kTcTma: full[grp][stage] mbarriers (<= 2 x 8)
   static constexpr int PBUF = MAG + (DSV_TC8_FILL ? 4096 : 0);  // tile-uniform phases: [group][2][D] float2
   static constexpr int RING = PBUF + 2 * 2 * D * 8;
   static constexpr int STAGE = 128 * D * 8;
@@ -105,10 +108,11 @@ __device__ __forceinline__ void issue_mma8(uint32_t sbase) {
 
 template <int K, bool PHASED, int MODE>
 __global__ void __launch_bounds__(256, 1)
-k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, const float4* __restrict__ tab,
-            float2* __restrict__ sv) {
+k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorMap tmap,
+            const uint4* __restrict__ bmat, const float4* __restrict__ tab, float2* __restrict__ sv) {
   using L = Tc8Layout<K>;
-  constexpr bool PAIR = MODE == kTcPair;
+  constexpr bool TMA = MODE == kTcTma;  // loads by tensor map; otherwise as kTcPair
+  constexpr bool PAIR = MODE == kTcPair || TMA;
   constexpr bool LOWT = MODE == kTcLow;
   constexpr bool ROW2 = MODE == kTcRow2;  // stage layout [member pair m][row] x 16 B
   constexpr int D = L::D;
@@ -137,6 +141,12 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
     mbar_init(sbase + L::BAR + 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (TMA && row == 0) {  // each group's TMA issuer owns its stage barriers (initialised before its first load)
+    for (int q = 0; q < S; ++q) mbar_init(sbase + L::TMABAR + 8 * (grp * S + q), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (TMA && tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+  static_assert(!TMA || 2 * S * 8 <= 192, "TMA barriers fit the barrier block");
   // gate digits, host layout [3 N0 rows][8 x 16 B] -> 128-byte swizzled rows
   for (int i = tid; i < 3 * N0 * 8; i += 256) {
     const int r = i / 8, c16 = i % 8;
@@ -158,7 +168,16 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
     if (tl < p.ntiles) {
       tb = expand(p.g, tl * 128);
       const uint32_t st0 = sbase + L::RING + ((grp * S) + (i % S)) * L::STAGE;
-      if constexpr (LOWT) {
+      if constexpr (TMA) {
+        if (row == 0) {  // the whole 128-row x 2^k-member tile in one bulk tensor load
+          int c[5];
+#pragma unroll
+          for (int q = 0; q < 5; ++q) c[q] = int(uint32_t(tl >> p.tma_shift[q]) & p.tma_mask[q]);
+          const uint32_t fb = sbase + L::TMABAR + 8 * (grp * S + (i % S));
+          mbar_expect_tx(fb, L::STAGE);
+          tma_load_5d(st0, &tmap, c, fb);
+        }
+      } else if constexpr (LOWT) {
 #pragma unroll
         for (int m = 0; m < D / 2; ++m) {
           const int q = row + 128 * m;
@@ -359,6 +378,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat, c
 #pragma unroll
     for (int s = 0; s + 1 < S - 1; ++s) tq[s] = tq[s + 1];
     tq[S - 2] = tb_new;
+    if constexpr (TMA) mbar_wait(sbase + L::TMABAR + 8 * (grp * S + stage), uint32_t(it / S) & 1u);
     const unsigned char* stg = sm + L::RING + (grp * S + stage) * L::STAGE;
     stage = stage + 1 == S ? 0 : stage + 1;
     float2 v[D];
@@ -952,11 +972,15 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
   p.tshift = -1;
 #endif
   for (int c = 0; c < 16; ++c) p.nib_shift[c] = d.nib_shift[c];
+  for (int q = 0; q < 5; ++q) {
+    p.tma_shift[q] = d.tma_shift[q];
+    p.tma_mask[q] = d.tma_mask[q];
+  }
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
   if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));
   int dev = 0;
   cudaGetDevice(&dev);
-  if (d.ws) {
+  if (MODE != kTcTma && d.ws) {
     using LW = Tc8WsLayout<K, PHASED>;
     const int smem = LW::BYTES + 1024;
     static bool attr_ws[64] = {false};
@@ -985,7 +1009,7 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
   const uint64_t need = (p.ntiles + 1) / 2;
   if (blocks > need) blocks = need;
   if (blocks == 0) return cudaSuccess;
-  k_dense_tc8<K, PHASED, MODE><<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+  k_dense_tc8<K, PHASED, MODE><<<unsigned(blocks), 256, smem, st>>>(p, d.tmap, static_cast<const uint4*>(d_bmat),
                                                                 static_cast<const float4*>(d_tab),
                                                                 static_cast<float2*>(sv));
   return cudaGetLastError();
@@ -998,6 +1022,7 @@ static cudaError_t tc8_k(const TcDesc& d, const void* d_bmat, const void* d_tab,
     case kTcPair: return ph ? tc8_go<K, true, kTcPair>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcPair>(d, d_bmat, d_tab, sv, st);
     case kTcLow: return ph ? tc8_go<K, true, kTcLow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcLow>(d, d_bmat, d_tab, sv, st);
     case kTcRow2: return ph ? tc8_go<K, true, kTcRow2>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcRow2>(d, d_bmat, d_tab, sv, st);
+    case kTcTma: return ph ? tc8_go<K, true, kTcTma>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcTma>(d, d_bmat, d_tab, sv, st);
   }
   return ph ? tc8_go<K, true, kTcRow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcRow>(d, d_bmat, d_tab, sv, st);
 }

@@ -109,6 +109,17 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
+// one TMA tile load (5-d tensor map, box in shared memory), completion counted in bytes on `bar`
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, const int (&c)[5], uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(dst),
+      "l"(tmap), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -204,6 +215,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 
 constexpr int kTcMaxNib = 10;                          // phase-table nibbles: index bits < 40
 constexpr int kTcRow = 0, kTcPair = 1, kTcLow = 2;     // tile copy modes (TcDesc::mode)
+constexpr int kTcTma = 4;   // tc8: like kTcPair (index bit 0 free) but tiles arrive by one TMA tensor load
 constexpr int kTcRow2 = 3;  // tc8: index bit 0 is the lowest target: members (2m, 2m+1) move as 16-byte pairs
 constexpr float kMagic = 12582912.f;   // 1.5 * 2^23: (x + kMagic) - kMagic = rint(x), |x| < 2^22
 constexpr float kMagic16 = 49152.f;    // 1.5 * 2^15: rounds to multiples of 2^-8, |x| < 2^14

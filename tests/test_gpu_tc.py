@@ -402,10 +402,12 @@ def test_wt_low_targets_vs_oracle(dtype):
 
 @pytest.mark.parametrize("targets", [(5, 6, 7, 8, 9), (2, 9, 15, 3, 12), (1, 4, 6, 9, 12), (0, 5, 9, 12, 14),
                                      (0, 1, 2, 3, 4), (0, 1, 2, 3), (0, 2, 5, 7)])
-def test_tc8_warp_specialised_kernel_all_layouts(targets):
-    """The warp-specialised int8-digit kernel (tc8.cu k_dense_tc8ws: loader /
-    converter / epilogue warps) forced on for every copy mode, plain and
-    phased, against the oracle and the two-group kernel."""
+def test_tc8_kernel_variants_all_layouts(targets):
+    """Every int8-digit kernel variant forced on for every copy mode, plain and
+    phased, against the oracle: the warp-specialised pipeline (tc8.cu
+    k_dense_tc8ws: loader / converter / epilogue warps), the two-group kernel
+    with per-thread cp.async copies, and the two-group kernel with TMA tile
+    loads (cp.async.bulk.tensor, mode kTcTma, where the layout allows)."""
     from paper_2308_01999_b200.fusion_fold import PhasedDenseGate
 
     rng = np.random.default_rng(sum(targets) + 31 * len(targets))
@@ -423,8 +425,9 @@ def test_tc8_warp_specialised_kernel_all_layouts(targets):
             want = want * np.exp(1j * ang)
         O.apply_dense(want, n, m, list(targets))
         outs = []
-        for ws in (1, 0):
+        for ws, tma in ((1, 1), (0, 0), (0, 1)):
             N.config_set("tc8ws", ws)
+            N.config_set("tma", tma)
             try:
                 sv = StateVector.from_amplitudes(st)
                 nat = _tc_launches(sv)
@@ -433,5 +436,6 @@ def test_tc8_warp_specialised_kernel_all_layouts(targets):
                 outs.append(sv.amplitudes)
             finally:
                 N.config_set("tc8ws", 1)
+                N.config_set("tma", 1)
         for o in outs:
             assert _rel_err(o, want) <= 2 * REL
