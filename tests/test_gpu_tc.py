@@ -1,12 +1,14 @@
-"""Tensor-core dense path (tc.cu: tcgen05 kind::tf32, 3-pass hi/lo split) on
-the B200 against the CPU oracle.
+"""Tensor-core dense path on the B200 against the CPU oracle.
 
-Complex64 dense windows with k = 4, 5, lowest target >= 2, index bit 0 free
-and >= 7 free bits take the tcgen05 kernel (plain and phased).  Bar (north_star): max|d| <= 1e-5
-for complex64; we also hold the error RELATIVE to the amplitude scale to
-5e-6 (fp32-level: measured 2.2e-6 worst case for k = 5, the tensor core's
-internal fp32 accumulation is not round-to-nearest), so a silently degraded
-1-pass TF32 product (~5e-4) fails.
+Complex64 dense / phased windows of k = 4, 5 (and 6, tc68.cu) run on
+tcgen05: by default the int8-digit kernels (tc8.cu: tcgen05.mma kind::i8 on
+exact 8-bit digits, int32 accumulation, A operand in TMEM — the two-group
+kernel with per-thread cp.async or TMA tile loads, and the warp-specialised
+pipeline), with DSV_TC8=0 the bf16-limb kernels (tc.cu / tc6.cu, kind::f16).
+Bar (north_star): max|d| <= 1e-5 for complex64; the error is also held
+RELATIVE to the amplitude scale to 5e-6 (the int8 digits drop products below
+2^-22 of the row scale: ~1.5e-6 per window), so a silently degraded 1-pass
+TF32 / bf16 product (~5e-4) fails.
 """
 
 import numpy as np
