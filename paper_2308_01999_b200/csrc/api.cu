@@ -61,6 +61,13 @@ bool g_tc8ws_env = [] {
   return !(e && e[0] == '0');
 }();
 
+// Launch-constant row phase vectors for windows whose row-varying phases sit
+// on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
+bool g_rowvec_env = [] {
+  const char* e = std::getenv("DSV_ROWVEC");
+  return !(e && e[0] == '0');
+}();
+
 // TMA tile loads for the int8-digit kernel's row-pair windows (tc8.cu kTcTma);
 // DSV_TMA=0 keeps the per-thread cp.async copies.
 bool g_tma_env = [] {
@@ -524,6 +531,27 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
         ++got;
       }
   }
+  std::vector<cplx<float>> m;
+  canon_matrix<float>(gg, matrix, m);
+  float bmax = 0.f;
+  for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
+  int e_b = 0;
+  if (bmax > 0.f) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
+  const bool use_tc8 = g_tc8_env && k <= 6 && e_b >= -20 && e_b <= 20;
+  // Row-varying phases on at most 3 tile-row bits (e.g. QFT-33's window on
+  // qubits 3..7, whose CP partners 0..2 are row bits): the row part of the
+  // phase depends only on those bits, so it is 2^nrb launch-constant vectors
+  // R_v[j] built here; the kernel multiplies them into the tile-uniform
+  // vector once per tile (nrb x 32 complex products in one warp) and every
+  // row then takes one complex product per member, as for tile-uniform
+  // windows, instead of a per-row 6-sincos tree.
+  std::vector<int> rb_bits;
+  for (const PhaseTerm& t : terms)
+    if ((row_mask >> t.bit & 1) && std::find(rb_bits.begin(), rb_bits.end(), t.bit) == rb_bits.end())
+      rb_bits.push_back(t.bit);
+  std::sort(rb_bits.begin(), rb_bits.end());
+  const bool rowvec = use_tc8 && k <= 5 && !rb_bits.empty() && rb_bits.size() <= 3 && g_rowvec_env;
+  auto in_rb = [&](int bit) { return rowvec && std::find(rb_bits.begin(), rb_bits.end(), bit) != rb_bits.end(); };
   // phase slots per index nibble: [nnib][16][8]; nibbles holding a term on a
   // row bit come first (d.nnib_row of them: the per-row lookups), the rest are
   // uniform over a tile (coop = no per-row nibble at all)
@@ -531,6 +559,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   for (int c = 0; c < 16; ++c) nib_of[c] = -1;
   uint32_t rowvar = 0, used = 0;
   for (const PhaseTerm& t : terms) {
+    if (in_rb(t.bit)) continue;
     const int c = t.bit / 4;
     if (c >= 10) return fail(DSV_EUNSUPPORTED, "tensor-core phase table covers index bits < 40");
     used |= 1u << c;
@@ -546,17 +575,31 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   d.coop = d.nnib_row == 0 ? 1 : 0;
   std::vector<double> tab(size_t(d.nnib) * 16 * 8, 0.0);
   for (const PhaseTerm& t : terms) {
+    if (in_rb(t.bit)) continue;
     const int ci = nib_of[t.bit / 4], bb = t.bit % 4;
     for (int v = 0; v < 16; ++v)
       if ((v >> bb) & 1) tab[(size_t(ci) * 16 + v) * 8 + t.slot] += t.th;
   }
-  std::vector<cplx<float>> m;
-  canon_matrix<float>(gg, matrix, m);
-  float bmax = 0.f;
-  for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
-  int e_b = 0;
-  if (bmax > 0.f) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
-  if (g_tc8_env && k <= 6 && e_b >= -20 && e_b <= 20) {
+  std::vector<float> rvec;  // [2^nrb][D] (cos, sin)
+  if (rowvec) {
+    d.nrb = int(rb_bits.size());
+    for (int q = 0; q < d.nrb; ++q) d.rb_bit[q] = rb_bits[q];
+    rvec.assign(size_t(2) * D << d.nrb, 0.f);
+    for (int v = 0; v < (1 << d.nrb); ++v)
+      for (int j = 0; j < D; ++j) {
+        double ang = 0.0;
+        for (const PhaseTerm& t : terms) {
+          if (!in_rb(t.bit)) continue;
+          const int q = int(std::find(rb_bits.begin(), rb_bits.end(), t.bit) - rb_bits.begin());
+          if (!((v >> q) & 1)) continue;
+          if (t.slot < k && !((j >> t.slot) & 1)) continue;
+          ang += t.th;
+        }
+        rvec[(size_t(v) * D + j) * 2] = float(std::cos(ang));
+        rvec[(size_t(v) * D + j) * 2 + 1] = float(std::sin(ang));
+      }
+  }
+  if (use_tc8) {
     // 8-bit digits (tc8.cu): X = B 2^(23 - e_b) rounded, X + 0x8080 split into
     // balanced base-256 digits b2 (2^16), b1 (2^8), b0 in [-128, 127];
     // rows [b2 | b1 | b0] x (n = 2i + out re/im), 128 bytes of K = 2j + in re/im
@@ -601,16 +644,19 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
         for (int l = 0; l < 3; ++l) host8[(size_t(l) * KK + n) * 128 + kk] = static_cast<unsigned char>(int8_t(dig[l]));
       }
     const size_t bbytes = (host8.size() + 255) / 256 * 256;
-    std::vector<unsigned char> host(bbytes + tab.size() * sizeof(float), 0);
+    const size_t tbytes = (tab.size() * sizeof(float) + 255) / 256 * 256;
+    std::vector<unsigned char> host(bbytes + tbytes + rvec.size() * sizeof(float), 0);
     std::memcpy(host.data(), host8.data(), host8.size());
     for (size_t i = 0; i < tab.size(); ++i) {
       const float f = float(tab[i]);
       std::memcpy(host.data() + bbytes + i * 4, &f, 4);
     }
+    if (!rvec.empty()) std::memcpy(host.data() + bbytes + tbytes, rvec.data(), rvec.size() * sizeof(float));
     if (int rc = ensure_gdata(s, host.size())) return rc;
     CK(cudaMemcpyAsync(s->gdata, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
     const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
     d.htab = reinterpret_cast<const float*>(host.data() + bbytes);
+    d.d_rvec = rvec.empty() ? nullptr : d_b + bbytes + tbytes;
     ProfTok t = prof_start(s);
     if (k == 6)
       CKL(launch_dense_tc68(d, d_b, d_b + bbytes, s->d, s->stream), 1);
@@ -821,7 +867,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tma", &g_tma_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)

@@ -58,6 +58,9 @@ struct TcDesc {
   // (cp.async.bulk.tensor) of this map over the state: dims = runs of row /
   // member / tile index bits, box = 128 rows x 2^k members ([member][row] in
   // shared memory); tile coordinates = bit fields of the tile index
+  int nrb;                // tc8 phased: tile-row bits carrying phase terms (<= 3), 0: none
+  int rb_bit[3];          // their amplitude index bits (row-phase vector v: bit q <-> rb_bit[q])
+  const void* d_rvec;     // [2^nrb][2^k] float2 launch-constant row phase vectors (device)
   CUtensorMap tmap;
   int tma_shift[5];          // coordinate of map dimension q = (tile >> shift[q]) & mask[q]
   uint32_t tma_mask[5];      // (mask 0: a row / member / padding dimension, coordinate 0)

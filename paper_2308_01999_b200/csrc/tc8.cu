@@ -60,6 +60,9 @@ struct Tc8P {
   float4 ctab[kTcMaxNib * 16 * 2];  // tile-uniform phase table (constant bank, broadcast reads)
   int tma_shift[5];       // kTcTma: tile coordinate of map dim q = (tile >> shift[q]) & mask[q]
   uint32_t tma_mask[5];
+  int nrb;                // row-phase bits (<= 3): per tile, 2^nrb vectors = tile vector x R_v
+  int rb_bit[3];
+  const float2* rvec;     // [2^nrb][D] launch-constant row phase factors
 };
 
 template <int K>
@@ -72,7 +75,10 @@ struct Tc8Layout {
   static constexpr int MAG = BAR + 256;           // 128 x 32 B of the accumulator start value (tcgen05.cp source)
   static constexpr int TMABAR = BAR + 64;         // kTcTma: full[grp][stage] mbarriers (<= 2 x 8)
   static constexpr int PBUF = MAG + (DSV_TC8_FILL ? 4096 : 0);  // tile-uniform phases: [group][2][D] float2
-  static constexpr int RING = PBUF + 2 * 2 * D * 8;
+  static constexpr int PBV = 8;                   // phase vectors per tile slot (2^nrb, nrb <= 3)
+  static constexpr int PBD = D + 1;               // vector stride (float2): rows of one warp read 8 vectors
+                                                  // at once, the pad puts them in different banks
+  static constexpr int RING = PBUF + 2 * 2 * PBV * PBD * 8;
   static constexpr int STAGE = 128 * D * 8;
   static constexpr int SMEM_MAX = 227 * 1024 - 1024;
   static constexpr int NS_FIT = (SMEM_MAX - RING) / (2 * STAGE);
@@ -162,6 +168,8 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
   const int prow = 2 * (row & 63);
   const int jpar = row >> 6;
   const uint64_t prowoff = expand(p.g, prow) ^ e0;
+  int vrow = 0;  // this row's value of the row-phase bits (rows are the same index bits in every tile)
+  for (int q = 0; q < p.nrb; ++q) vrow |= int((rowoff >> p.rb_bit[q]) & 1u) << q;
   auto issue = [&](int i) -> uint64_t {
     const uint64_t tl = tile_of(i);
     uint64_t tb = 0;
@@ -218,7 +226,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
     cp_async_commit();
     return tb;
   };
-  float2* Pb = reinterpret_cast<float2*>(sm + L::PBUF) + grp * 2 * D;
+  float2* Pb = reinterpret_cast<float2*>(sm + L::PBUF) + grp * 2 * L::PBV * L::PBD;
   auto coop_phase = [&](int i, uint64_t tb) {
     const int j = row - (128 - D);
     if (PHASED && !p.coop && j == 0 && tile_of(i) < p.ntiles) {
@@ -234,7 +242,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
           a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
         }
       }
-      float4* hb = reinterpret_cast<float4*>(Pb + (i & 1) * D);
+      float4* hb = reinterpret_cast<float4*>(Pb + (i & 1) * L::PBV * L::PBD);
       hb[0] = make_float4(a[0], a[1], a[2], a[3]);
       hb[1] = make_float4(a[4], a[5], a[6], a[7]);
     }
@@ -256,7 +264,14 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
       for (int m = 0; m < K; ++m) ang += ((j >> m) & 1) ? a[m] : 0.f;
       float sn, cs;
       sincos_unit(ang, &sn, &cs);
-      Pb[(i & 1) * D + j] = make_float2(cs, sn);
+      if (p.nrb == 0) {
+        Pb[(i & 1) * L::PBV * L::PBD + j] = make_float2(cs, sn);
+      } else {  // one vector per value of the row-phase bits: tile vector x launch-constant row factor
+        for (int v = 0; v < (1 << p.nrb); ++v) {
+          const float2 r = __ldg(p.rvec + v * D + j);
+          Pb[((i & 1) * L::PBV + v) * L::PBD + j] = make_float2(cs * r.x - sn * r.y, cs * r.y + sn * r.x);
+        }
+      }
     }
   };
   uint64_t tq[S - 1];
@@ -403,7 +418,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
     }
     if constexpr (PHASED) {
       if (p.coop) {
-        const float2* P = Pb + (it & 1) * D;
+        const float2* P = Pb + ((it & 1) * L::PBV + vrow) * L::PBD;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           const float2 x = v[j], f = P[j];
@@ -411,7 +426,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
         }
       } else {
         float a[8];
-        const float4* hb = reinterpret_cast<const float4*>(Pb + (it & 1) * D);
+        const float4* hb = reinterpret_cast<const float4*>(Pb + (it & 1) * L::PBV * L::PBD);
         const float4 h0 = hb[0], h1 = hb[1];
         a[0] = h0.x + ra[0]; a[1] = h0.y + ra[1]; a[2] = h0.z + ra[2]; a[3] = h0.w + ra[3];
         a[4] = h1.x + ra[4]; a[5] = h1.y + ra[5]; a[6] = h1.z + ra[6]; a[7] = h1.w + ra[7];
@@ -976,6 +991,9 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
     p.tma_shift[q] = d.tma_shift[q];
     p.tma_mask[q] = d.tma_mask[q];
   }
+  p.nrb = d.nrb;
+  for (int q = 0; q < 3; ++q) p.rb_bit[q] = d.rb_bit[q];
+  p.rvec = static_cast<const float2*>(d.d_rvec);
   for (int j = 0; j < (1 << K); ++j) p.offs[j] = d.offs[j];
   if (d.htab && d.nnib > 0) std::memcpy(p.ctab, d.htab, size_t(d.nnib) * 16 * 2 * sizeof(float4));
   int dev = 0;
@@ -1017,7 +1035,7 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
 
 template <int K>
 static cudaError_t tc8_k(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st) {
-  const bool ph = d.nnib > 0;
+  const bool ph = d.nnib > 0 || d.nrb > 0;
   switch (d.mode) {
     case kTcPair: return ph ? tc8_go<K, true, kTcPair>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcPair>(d, d_bmat, d_tab, sv, st);
     case kTcLow: return ph ? tc8_go<K, true, kTcLow>(d, d_bmat, d_tab, sv, st) : tc8_go<K, false, kTcLow>(d, d_bmat, d_tab, sv, st);
