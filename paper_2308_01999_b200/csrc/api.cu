@@ -60,6 +60,8 @@ bool g_tc8ws_env = [] {
   const char* e = std::getenv("DSV_TC8WS");
   return !(e && e[0] == '0');
 }();
+bool g_tc8ws_all = false;  // A/B: the warp-specialised pipeline for every plain tc8 window
+bool g_tc8ws_row2 = true;  // A/B: ... for windows with index bit 0 the lowest target
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -623,19 +625,26 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     }
     d.e_b = e_b;
     // warp-specialised pipeline only where it measured faster on the same box
-    // (tools/_patt2.py, tools/_ab_qft.py at n = 33): plain windows with index
-    // bit 0 the lowest target, whose member pairs move as 16-byte units
-    // (0.87-0.89 -> 0.97 of the copy peak).  Elsewhere it is a wash or up to
-    // 4 % slower (contiguous and phased windows, most scattered-target QV
-    // windows): DSV_TC8WS=0 disables it, and the kernel stays available for
-    // A/B through dsv_config_set("tc8ws", ...).
-    d.ws = (g_tc8ws_env && terms.empty() && d.mode == 3) ? 1 : 0;
+    // (tools/_patt2.py, _ab_qft.py, _ab_qvwin.py at n = 33): plain windows
+    // with index bit 0 the lowest target (member pairs as 16-byte units,
+    // 0.87-0.89 -> 0.97 of the copy peak) or with the lowest target at bit 1
+    // or 2 (QV windows 34.0 -> 31.1 ms and 28.3 -> 27.5 ms).  Elsewhere it is
+    // a wash or up to 5 % slower (contiguous and phased windows, targets from
+    // bit 3 up): DSV_TC8WS=0 disables it; dsv_config_set("tc8ws_all", 1)
+    // forces it for A/B runs.
+    const bool ws_layout = (d.mode == 3 && g_tc8ws_row2) || (d.mode == 1 && gg.tsorted[0] <= 2);
+    d.ws = (g_tc8ws_env && terms.empty() && (ws_layout || g_tc8ws_all)) ? 1 : 0;
     // TMA tile loads where they measured faster than the per-thread cp.async
     // copies (tools/_ab_tma.py, same box, n = 33): windows whose 128 tile rows
     // are split around the targets (lowest target below bit 7, e.g. QFT-33's
     // window on qubits 3..7: 27.5 -> 27.1 ms).  Rows that are one contiguous
     // run (plain windows high up: 22.5 -> 24.4 ms) keep cp.async.
-    if (k <= 5 && d.mode == 1 && gg.tsorted[0] < 7 && build_tile_tmap(s, gg, &d)) d.mode = 4;  // kTcTma
+    // The box's innermost run is the rows below the lowest target: under
+    // 64 bytes (lowest target bit 1 or 2) TMA moves 16-32-byte pieces and
+    // was measured slower (QV windows with targets from bit 1: 31 -> 34.8
+    // ms), so those keep cp.async with the row-pair mapping of tc8.cu.
+    if (k <= 5 && d.mode == 1 && gg.tsorted[0] >= 3 && gg.tsorted[0] < 7 && build_tile_tmap(s, gg, &d))
+      d.mode = 4;  // kTcTma
     std::vector<unsigned char> host8(size_t(3) * KK * 128, 0);
     for (int n = 0; n < KK; ++n)
       for (int kk = 0; kk < KK; ++kk) {
@@ -867,7 +876,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2}, {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)

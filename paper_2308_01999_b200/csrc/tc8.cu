@@ -56,6 +56,7 @@ struct Tc8P {
   int nnib_row;           // leading nibbles that vary over the rows (the rest: tile-uniform sums)
   int nib_shift[16];      // amplitude-index shift of nibble c
   int tshift;             // member j at offset j << tshift (contiguous targets), else -1: offs[]
+  int jpos;               // row-pair copies: thread-index bit that selects the member parity (see issue())
   uint64_t offs[1 << K];  // member offsets (amplitudes)
   float4 ctab[kTcMaxNib * 16 * 2];  // tile-uniform phase table (constant bank, broadcast reads)
   int tma_shift[5];       // kTcTma: tile coordinate of map dim q = (tile >> shift[q]) & mask[q]
@@ -165,8 +166,12 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
   auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + (2 * uint64_t(i) + grp) * step; };
   const uint64_t e0 = expand(p.g, 0);
   const uint64_t rowoff = expand(p.g, row) ^ e0;
-  const int prow = 2 * (row & 63);
-  const int jpar = row >> 6;
+  // row-pair copies: thread-index bit jpos picks the member parity, the other
+  // six bits the row pair.  jpos = (lowest target - 1) capped at 6, so a
+  // warp's 16-byte copies cover whole contiguous runs (with the lowest target
+  // at bit 1 adjacent threads take the two members of one 32-byte sector).
+  const int prow = 2 * ((row & ((1 << p.jpos) - 1)) | ((row >> (p.jpos + 1)) << p.jpos));
+  const int jpar = (row >> p.jpos) & 1;
   const uint64_t prowoff = expand(p.g, prow) ^ e0;
   int vrow = 0;  // this row's value of the row-phase bits (rows are the same index bits in every tile)
   for (int q = 0; q < p.nrb; ++q) vrow |= int((rowoff >> p.rb_bit[q]) & 1u) << q;
@@ -647,7 +652,7 @@ k_dense_tc8ws(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat,
       for (int rr = 0; rr < 2; ++rr) {
       const int row = tid + 64 * rr;  // this loader's two rows
       const uint64_t rowoff = expand(p.g, row) ^ e0;
-      const int prow = 2 * (row & 63);
+      const int prow = 2 * (row & 63);  // (the jpos mapping measured slower in this pipeline)
       const int jpar = row >> 6;
       const uint64_t prowoff = expand(p.g, prow) ^ e0;
       if constexpr (LOWT) {
@@ -983,6 +988,15 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
   p.coop = d.coop;
   p.nnib_row = d.nnib_row;
   p.tshift = d.tshift;
+  p.jpos = 6;
+  {  // lowest target bit (the first hole above bit 0 in PAIR mode): member parity sits at thread bit t - 1
+    int lo = 64;
+    for (int j = 1; j < (1 << K); ++j) {
+      const uint64_t o = d.offs[j];
+      if (o) lo = std::min(lo, __builtin_ctzll(o));
+    }
+    if (lo >= 1 && lo <= 7) p.jpos = lo - 1;
+  }
 #ifdef DSV_TC8_NOSTRIDE
   p.tshift = -1;
 #endif
