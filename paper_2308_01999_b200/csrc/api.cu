@@ -21,6 +21,7 @@
 #include <vector>
 
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/dsv.h"
 #include "common.cuh"
@@ -136,6 +137,24 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #expr);  \
     g_launches += (n);                                   \
   } while (0)
+
+// NVTX ranges around the C-ABI entry points (names = the entry point), so an
+// nsys / ncu --nvtx timeline lines kernels up with the calls that issued them.
+// Off unless DSV_NVTX=1 (the push/pop pair is cheap, but not free per gate).
+const bool g_nvtx_env = [] {
+  const char* e = std::getenv("DSV_NVTX");
+  return e && e[0] == '1';
+}();
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(g_nvtx_env) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+#define DSV_NVTX_RANGE() NvtxRange nvtx_range_(__func__)
 
 struct DeviceGuard {
   int prev = -1;
@@ -1139,6 +1158,7 @@ int dsv_copy(dsv_state* dst, const dsv_state* src) {
 
 int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, int k,
                      const int32_t* cb, const int32_t* cv, int nctrl) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!matrix) return fail(DSV_EINVAL, "null matrix");
   GateGeom gg;
@@ -1324,6 +1344,7 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
 int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* targets, int k,
                             const int32_t* cross_t, const int32_t* cross_b, const double* cross_theta,
                             int ncross, const int32_t* out_b, const double* out_theta, int nout) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!matrix) return fail(DSV_EINVAL, "null matrix");
   if (k < 1 || k > 6) return fail(DSV_EUNSUPPORTED, "phased window arity %d outside [1, 6]", k);
@@ -1421,6 +1442,7 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
 
 int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const int32_t* targets,
                       int k, const int32_t* cb, const int32_t* cv, int nctrl) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!perm || !diag) return fail(DSV_EINVAL, "null permutation/diagonal");
   GateGeom gg;
@@ -1676,6 +1698,7 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
 
 int dsv_apply_pauli_rotation(dsv_state* s, double theta, double coef_re, double coef_im,
                              const int32_t* bits, const char* paulis, int m) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   PauliMasks pm;
   if (int rc = parse_pauli(s, bits, paulis, m, &pm)) return rc;
@@ -1699,6 +1722,7 @@ int dsv_apply_pauli_rotation(dsv_state* s, double theta, double coef_re, double 
 }
 
 int dsv_apply_pauli_product(dsv_state* s, const int32_t* bits, const char* paulis, int m) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   PauliMasks pm;
   if (int rc = parse_pauli(s, bits, paulis, m, &pm)) return rc;
@@ -1719,6 +1743,7 @@ int dsv_apply_pauli_product(dsv_state* s, const int32_t* bits, const char* pauli
 // ---- layout -----------------------------------------------------------------------------
 
 int dsv_swap_index_bits(dsv_state* s, const int32_t* pairs, int npairs) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (npairs < 0) return fail(DSV_EINVAL, "negative pair count");
   uint64_t seen = 0;
@@ -1806,6 +1831,7 @@ static int check_ordering(const dsv_state* s, const int32_t* ordering) {
 static const uint64_t kAccessChunk = 1ull << 25;
 
 int dsv_access_get(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64_t end, void* host_out) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (int rc = check_ordering(s, ordering)) return rc;
   if (!(begin < end && end <= namps(s))) return fail(DSV_EINVAL, "bad range [%llu, %llu)",
@@ -1827,6 +1853,7 @@ int dsv_access_get(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64
 }
 
 int dsv_access_set(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64_t count, const void* host_in) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (int rc = check_ordering(s, ordering)) return rc;
   if (count == 0 || begin >= namps(s) || count > namps(s) - begin) return fail(DSV_EINVAL, "range exceeds state size");
@@ -1953,18 +1980,21 @@ static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2,
 }
 
 int dsv_norm2(dsv_state* s, double* out) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   DeviceGuard g(s->device);
   return probs_impl(s, nullptr, 0, true, out, nullptr, nullptr);
 }
 
 int dsv_marginal_probs(dsv_state* s, const int32_t* bits, int k, double* out) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   DeviceGuard g(s->device);
   return probs_impl(s, bits, k, true, out, nullptr, nullptr);
 }
 
 int dsv_expect_pauli(dsv_state* s, const int32_t* bits, const char* paulis, int m, double* out) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   PauliMasks pm;
   if (int rc = parse_pauli(s, bits, paulis, m, &pm)) return rc;
@@ -1989,6 +2019,7 @@ int dsv_expect_pauli(dsv_state* s, const int32_t* bits, const char* paulis, int 
 }
 
 int dsv_inner(dsv_state* a, const dsv_state* b, double* out) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(a)) return rc;
   if (int rc = check_state(b)) return rc;
   if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "inner product of states with different shape");
@@ -2009,6 +2040,7 @@ int dsv_inner(dsv_state* a, const dsv_state* b, double* out) {
 }
 
 int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, int k, double* out) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!matrix) return fail(DSV_EINVAL, "null matrix");
   GateGeom gg;
@@ -2050,6 +2082,7 @@ int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, 
 }
 
 int dsv_collapse(dsv_state* s, const int32_t* bits, int k, uint64_t outcome, double norm2_kept) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!(norm2_kept > 0.0)) return fail(DSV_EINVAL, "collapse onto a zero-probability outcome");
   uint64_t mask = 0, val = 0;
@@ -2082,6 +2115,7 @@ int dsv_scale(dsv_state* s, double factor) {
 }
 
 int dsv_sample(dsv_state* s, const double* variates, int64_t shots, uint64_t* outcomes) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (shots < 1) return fail(DSV_EINVAL, "shots must be >= 1");
   DeviceGuard g(s->device);
@@ -2132,6 +2166,7 @@ int dsv_sample(dsv_state* s, const double* variates, int64_t shots, uint64_t* ou
 // ---- segments -----------------------------------------------------------------------------
 
 int dsv_exchange_halves(dsv_state* a, dsv_state* b, int local_bit, int part, int nparts) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(a)) return rc;
   if (int rc = check_state(b)) return rc;
   if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "exchange between segments of different shape");
@@ -2156,6 +2191,7 @@ int dsv_exchange_halves(dsv_state* a, dsv_state* b, int local_bit, int part, int
 }
 
 int dsv_exchange_all(dsv_state* a, dsv_state* b) {
+  DSV_NVTX_RANGE();
   if (int rc = check_state(a)) return rc;
   if (int rc = check_state(b)) return rc;
   if (a->nbits != b->nbits || a->dtype != b->dtype) return fail(DSV_EINVAL, "exchange between segments of different shape");
@@ -2233,6 +2269,7 @@ int run_masked(dsv_state* run, dsv_state* a, dsv_state* b, const MaskedPlan& mp,
 
 int dsv_exchange_masked(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b,
                         int part, int nparts) {
+  DSV_NVTX_RANGE();
   MaskedPlan mp;
   if (int rc = plan_masked(a, b, lbits, q, pat_a, pat_b, &mp)) return rc;
   if (nparts < 1 || part < 0 || part >= nparts) return fail(DSV_EINVAL, "bad exchange slice %d/%d", part, nparts);
@@ -2248,6 +2285,7 @@ int dsv_exchange_masked(dsv_state* a, dsv_state* b, const int32_t* lbits, int q,
 }
 
 int dsv_exchange_pair(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b) {
+  DSV_NVTX_RANGE();
   MaskedPlan mp;
   if (int rc = plan_masked(a, b, lbits, q, pat_a, pat_b, &mp)) return rc;
   if (a->ipc || b->ipc) return fail(DSV_EINVAL, "dsv_exchange_pair needs two local segments (use dsv_exchange_masked)");
