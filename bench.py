@@ -432,10 +432,12 @@ def run_single(args) -> None:
     legs = {}
     clocks2 = ClockSampler(dev).start()
     time.sleep(0.2)
+    from paper_2308_01999_b200.fusion_cluster import fuse_auto
+
     qv_gates = to_gates(gen_qv(N_QUBITS, 30, seed=0))
-    qv_ops = fuse_fold(qv_gates, FOLD_K).ops
+    qv_ops = fuse_auto(qv_gates, FOLD_K).ops  # cluster fuser: 134 windows (fold / reference: 152)
     rnd = random_gate_sequence(N_QUBITS, 200, np.random.default_rng(0), max_arity=2)
-    for name, circ, lops in (("qv33_c64_fold5", qv_gates, qv_ops), ("random33_c64", rnd, rnd)):
+    for name, circ, lops in (("qv33_c64_fused5", qv_gates, qv_ops), ("random33_c64", rnd, rnd)):
         step(lops)
         nat.event_record(2)
         step(lops)
@@ -607,10 +609,10 @@ def run_sharded(args) -> None:
     if (not virtual or shift > 0) and not args.skip_legs:
         if P in (2, 4):
             # BASELINE config 4: QV-34 depth 30, complex128 (256 GiB), fold fuser k = 4
-            from paper_2308_01999_b200.fusion_fold import fuse_fold
+            from paper_2308_01999_b200.fusion_cluster import fuse_auto
 
             qv = to_gates(gen_qv(34 - shift, 30, seed=0))
-            qv_ops = fuse_fold(qv, 4).ops
+            qv_ops = fuse_auto(qv, 4).ops  # cluster fuser at k = 4: 188 windows (reference: 232)
             s4 = ShardedStateVector(34 - shift, devices, np.complex128)
             s4.prof(True)
             ms = _sharded_time(s4, qv_ops, 1, 1)

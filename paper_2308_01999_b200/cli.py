@@ -90,11 +90,12 @@ def fused_ops(args, gates, counters: dict, timings: dict):
     t0 = time.perf_counter()
     if args.fusion:
         kind, _, k = args.fusion.partition(":")
-        if kind != "fold":
-            raise InvalidArgumentError(f"unknown fusion {args.fusion!r} (use fold:K)")
+        if kind not in ("fold", "cluster", "auto"):
+            raise InvalidArgumentError(f"unknown fusion {args.fusion!r} (use fold:K, cluster:K or auto:K)")
+        from .fusion_cluster import fuse_auto, fuse_cluster
         from .fusion_fold import fuse_fold
 
-        fc = fuse_fold(gates, int(k or 5))
+        fc = {"fold": fuse_fold, "cluster": fuse_cluster, "auto": fuse_auto}[kind](gates, int(k or 5))
         ops = fc.ops
         counters["data_passes"] = fc.data_passes
     elif args.max_fused_gate_size or args.max_fused_diagonal_gate_size:
@@ -263,7 +264,8 @@ def build_parser() -> argparse.ArgumentParser:
     sim.add_argument("--workers", type=int, default=default_workers())
     sim.add_argument("--max-fused-gate-size", type=int, default=None)
     sim.add_argument("--max-fused-diagonal-gate-size", type=int, default=None)
-    sim.add_argument("--fusion", default=None, help="fold:K — the phase-folding fuser with K-qubit windows")
+    sim.add_argument("--fusion", default=None,
+                     help="fold:K (phase-folding fuser), cluster:K (cluster-merging fuser) or auto:K (fewer passes of the two)")
     sim.add_argument("--dtype", choices=sorted(DTYPES), default="c128")
     sim.add_argument("--device", type=int, default=None)
     sim.add_argument("--gpus", type=int, default=1, help="shard the state over N GPUs (one host process)")

@@ -144,3 +144,12 @@ def test_gpus_flag_shards_and_verifies(capsys, gpu_available):
     assert rep["verification"]["passed"]
     assert rep["params"]["gpus"] == 4
     assert rep["counters"]["transfer_stats"]["num_reorders"] > 0
+
+
+@pytest.mark.gpu
+def test_cluster_fusion_flag(capsys, gpu_available):
+    code, rep = run_json(capsys, "simulate", "--circuit", "qv", "--n", "12", "--dtype", "c128", "--fusion", "auto:4",
+                         "--verify")
+    assert code == 0
+    assert rep["verification"]["passed"]
+    assert rep["counters"]["data_passes"] < rep["counters"]["gates"]

@@ -30,6 +30,7 @@ import numpy as np  # noqa: E402
 import bench  # noqa: E402
 from paper_2308_01999_b200.circuits import gen_qft, gen_qv, random_gate_sequence, to_gates  # noqa: E402
 from paper_2308_01999_b200.fusion import FusionConfig, fuse  # noqa: E402
+from paper_2308_01999_b200.fusion_cluster import fuse_auto  # noqa: E402
 from paper_2308_01999_b200.fusion_fold import fuse_fold  # noqa: E402
 from paper_2308_01999_b200.statevec import StateVector  # noqa: E402
 
@@ -133,7 +134,9 @@ def main():
         26, CPU_GATES, np.random.default_rng(0), max_arity=2)), np.complex64, full_n=30, full_count=200)
     # ---- config 4 per GPU: QV-33 complex128 fold k = 4 (one of the two 2^33 segments of QV-34 on 2 GPUs)
     g4 = to_gates(gen_qv(33, 30, seed=0))
-    rows["4_qv33_c128_per_gpu"] = {"gpu_fold_k4": gpu_run(33, fuse_fold(g4, 4).ops, np.complex128, len(g4), reps=1)}
+    rows["4_qv33_c128_per_gpu"] = {"gpu_cluster_k4": gpu_run(33, fuse_auto(g4, 4).ops, np.complex128, len(g4), reps=1),
+                                   "windows_cluster_k4": fuse_auto(g4, 4).data_passes,
+                                   "windows_fold_k4": fuse_fold(g4, 4).data_passes}
     rows["4_qv33_c128_per_gpu"]["cpu_reference"] = cpu_ref(
         26, ref_gates("qv", 26)[:CPU_GATES], np.complex128, full_n=34, full_count=510)
     # ---- config 5 per GPU: random-33 complex64 (one of the 8 segments of random-36)
