@@ -96,8 +96,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap", "utilization.gpu")
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, gpu_index):
+        # one index or a list (N > 1: every GPU of the run is sampled)
+        self.gpu = ",".join(str(g) for g in sorted(set(gpu_index))) if isinstance(gpu_index, (list, tuple)) else gpu_index
         self.rows: list[list[str]] = []
         self._proc = None
         self._thread = None
@@ -548,10 +549,58 @@ def _exchange_gbs(profs) -> dict:
             "link_GB_per_s_per_device_per_direction": by / 4.0 / (ms / 1000.0) / 1e9}
 
 
+def _run_legs(legs: dict, P: int, devices, shift: int) -> None:
+    """BASELINE configs 4 and 5 on the N > 1 run (see run_sharded)."""
+    from paper_2308_01999_b200.circuits import gen_qv, random_gate_sequence, to_gates
+    from paper_2308_01999_b200.fusion_cluster import fuse_auto
+    from paper_2308_01999_b200.gates import PauliString
+    from paper_2308_01999_b200.shard import ShardedStateVector
+
+    if P in (2, 4):
+        # BASELINE config 4: QV-34 depth 30, complex128 (256 GiB), k = 4 windows
+        qv = to_gates(gen_qv(34 - shift, 30, seed=0))
+        qv_ops = fuse_auto(qv, 4).ops  # cluster fuser at k = 4: 181 windows (reference: 232)
+        s4 = ShardedStateVector(34 - shift, devices, np.complex128)
+        s4.prof(True)
+        ms = _sharded_time(s4, qv_ops, 1, 1)
+        pf = s4.prof_read()
+        legs["qv34_c128"] = {"n_qubits": 34 - shift, "gates_per_s": len(qv) / (ms / 1000.0), "ms_per_circuit": ms,
+                             "circuit_gates": len(qv), "fused_ops": len(qv_ops),
+                             "transfer_stats": s4.stats.as_dict(), "norm": s4.norm_squared(),
+                             "exchange": _exchange_gbs(pf)}
+        s4.close()
+        del s4
+    if P in (4, 8):
+        # BASELINE config 5: random-36 c64 (512 GiB) + expectation values;
+        # weak-scaling efficiency against the same generator at 33 qubits on 1 GPU
+        n5 = 36 - shift
+        rnd36 = random_gate_sequence(n5, 200, np.random.default_rng(0), max_arity=2)
+        s5 = ShardedStateVector(n5, devices, np.complex64)
+        s5.prof(True)
+        ms36 = _sharded_time(s5, rnd36, 1, 1)
+        pf = s5.prof_read()
+        t0 = time.perf_counter()
+        ev = s5.expectation([PauliString(((0, "Z"), (17, "X"), (n5 - 1, "Y")))])
+        zsum = s5.expectation([PauliString(((q, "Z"),)) for q in range(n5)])
+        ev_s = time.perf_counter() - t0
+        leg = {"n_qubits": n5, "gates_per_s": len(rnd36) / (ms36 / 1000.0), "ms_per_circuit": ms36,
+               "circuit_gates": len(rnd36), "transfer_stats": s5.stats.as_dict(),
+               "expect_Z0X17Y35": [ev.real, ev.imag], "sum_Zq": zsum.real, "expectation_s": ev_s,
+               "norm": s5.norm_squared(), "exchange": _exchange_gbs(pf)}
+        s5.close()
+        del s5
+        if P == 8:
+            rnd33 = random_gate_sequence(n5 - 3, 200, np.random.default_rng(0), max_arity=2)
+            s1 = ShardedStateVector(n5 - 3, [devices[0]], np.complex64)
+            ms33 = _sharded_time(s1, rnd33, 1, 1)
+            s1.close()
+            del s1
+            leg["weak_scaling"] = {"T33_1gpu_ms": ms33, "T36_8gpu_ms": ms36, "efficiency": ms33 / ms36}
+        legs["random36_c64"] = leg
+
+
 def run_sharded(args) -> None:
     from paper_2308_01999_b200 import _native as N
-    from paper_2308_01999_b200.circuits import gen_qv, random_gate_sequence, to_gates
-    from paper_2308_01999_b200.gates import PauliString
     from paper_2308_01999_b200.shard import ShardedStateVector
 
     ndev = N.device_count()
@@ -562,7 +611,7 @@ def run_sharded(args) -> None:
     devices = [d % ndev for d in range(P)]
     gates, ops, fuse_s = workload(args.fusion)
     sv = ShardedStateVector(N_QUBITS, devices, np.complex64)
-    clocks = ClockSampler(devices[0]).start()
+    clocks = ClockSampler(devices).start()
     time.sleep(0.3)
     sv.prof(True)
     launches0 = N.launch_count()
@@ -607,49 +656,10 @@ def run_sharded(args) -> None:
     # a 1-GPU box, where the segments share one device)
     shift = int(os.environ.get("DSV_BENCH_LEG_SHIFT", "0"))
     if (not virtual or shift > 0) and not args.skip_legs:
-        if P in (2, 4):
-            # BASELINE config 4: QV-34 depth 30, complex128 (256 GiB), fold fuser k = 4
-            from paper_2308_01999_b200.fusion_cluster import fuse_auto
-
-            qv = to_gates(gen_qv(34 - shift, 30, seed=0))
-            qv_ops = fuse_auto(qv, 4).ops  # cluster fuser at k = 4: 181 windows (reference: 232)
-            s4 = ShardedStateVector(34 - shift, devices, np.complex128)
-            s4.prof(True)
-            ms = _sharded_time(s4, qv_ops, 1, 1)
-            pf = s4.prof_read()
-            legs["qv34_c128"] = {"n_qubits": 34 - shift, "gates_per_s": len(qv) / (ms / 1000.0), "ms_per_circuit": ms,
-                                 "circuit_gates": len(qv), "fused_ops": len(qv_ops),
-                                 "transfer_stats": s4.stats.as_dict(), "norm": s4.norm_squared(),
-                                 "exchange": _exchange_gbs(pf)}
-            s4.close()
-            del s4
-        if P in (4, 8):
-            # BASELINE config 5: random-36 c64 (512 GiB) + expectation values;
-            # weak-scaling efficiency against the same generator at 33 qubits on 1 GPU
-            n5 = 36 - shift
-            rnd36 = random_gate_sequence(n5, 200, np.random.default_rng(0), max_arity=2)
-            s5 = ShardedStateVector(n5, devices, np.complex64)
-            s5.prof(True)
-            ms36 = _sharded_time(s5, rnd36, 1, 1)
-            pf = s5.prof_read()
-            t0 = time.perf_counter()
-            ev = s5.expectation([PauliString(((0, "Z"), (17, "X"), (n5 - 1, "Y")))])
-            zsum = s5.expectation([PauliString(((q, "Z"),)) for q in range(n5)])
-            ev_s = time.perf_counter() - t0
-            leg = {"n_qubits": n5, "gates_per_s": len(rnd36) / (ms36 / 1000.0), "ms_per_circuit": ms36,
-                   "circuit_gates": len(rnd36), "transfer_stats": s5.stats.as_dict(),
-                   "expect_Z0X17Y35": [ev.real, ev.imag], "sum_Zq": zsum.real, "expectation_s": ev_s,
-                   "norm": s5.norm_squared(), "exchange": _exchange_gbs(pf)}
-            s5.close()
-            del s5
-            if P == 8:
-                rnd33 = random_gate_sequence(n5 - 3, 200, np.random.default_rng(0), max_arity=2)
-                s1 = ShardedStateVector(n5 - 3, [devices[0]], np.complex64)
-                ms33 = _sharded_time(s1, rnd33, 1, 1)
-                s1.close()
-                del s1
-                leg["weak_scaling"] = {"T33_1gpu_ms": ms33, "T36_8gpu_ms": ms36, "efficiency": ms33 / ms36}
-            legs["random36_c64"] = leg
+        try:
+            _run_legs(legs, P, devices, shift)
+        except Exception as e:  # a leg must not cost the main line
+            legs["error"] = f"{type(e).__name__}: {e}"[:400]
 
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": P, "steps": args.steps,

@@ -62,7 +62,9 @@ bool g_tc8ws_env = [] {
   return !(e && e[0] == '0');
 }();
 bool g_tc8ws_all = false;  // A/B: the warp-specialised pipeline for every plain tc8 window
-bool g_tc8ws_row2 = true;  // A/B: ... for windows with index bit 0 the lowest target
+bool g_tc8ws_row2 = true;
+bool g_tc4_all = false;
+bool g_wt4 = false;  // A/B: complex64 k = 4 gates inside bits 0..5 on the warp-transpose kernel  // A/B: every complex64 k = 4 dense gate on the tensor cores  // A/B: ... for windows with index bit 0 the lowest target
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -895,7 +897,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2}, {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)
