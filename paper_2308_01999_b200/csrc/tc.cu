@@ -138,8 +138,8 @@ k_dense_tc(const __grid_constant__ TcP<K> p, const uint4* __restrict__ bmat, con
   const uint32_t sbase = (raw_base + 1023u) & ~1023u;
   unsigned char* sm = smem_raw + (sbase - raw_base);
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int grp = tid >> 7;   // consumer group
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform (TMEM addresses in uniform registers)
+  const int grp = warp >> 2;  // consumer group
   const int row = tid & 127;  // TMEM lane = tile row = amplitude group within the tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);
   const uint32_t bar = sbase + L::BAR + 8 * grp;

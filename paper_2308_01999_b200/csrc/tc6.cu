@@ -87,7 +87,7 @@ k_dense_tc6(const __grid_constant__ Tc6P p, const uint4* __restrict__ bmat, cons
   const uint32_t sbase = (raw_base + 1023u) & ~1023u;
   unsigned char* sm = smem_raw + (sbase - raw_base);
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform (TMEM addresses in uniform registers)
   const int row = tid & 127;
   const int half = tid >> 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);

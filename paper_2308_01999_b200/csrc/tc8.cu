@@ -130,8 +130,11 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
   const uint32_t sbase = (raw_base + 1023u) & ~1023u;
   unsigned char* sm = smem_raw + (sbase - raw_base);
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int grp = tid >> 7;
+  // warp / group index through a lane-0 shuffle: provably warp-uniform, so the
+  // TMEM addresses derived from it live in uniform registers (ncu showed ~2.5
+  // R2UR per amplitude moving them there for every tcgen05.ld / st)
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int grp = warp >> 2;
   const int row = tid & 127;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);
   const uint32_t bar = sbase + L::BAR + 8 * grp;
@@ -592,7 +595,7 @@ k_dense_tc8ws(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat,
   const uint32_t sbase = (raw_base + 1023u) & ~1023u;
   unsigned char* sm = smem_raw + (sbase - raw_base);
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform (TMEM addresses in uniform registers)
   const int role = warp < 2 ? 0 : (warp < 6 ? 1 : 2);
   // converters / epilogue: the row is this thread's TMEM lane (quarter = warp % 4)
   const int row = role == 0 ? tid : (((warp & 3) << 5) | (tid & 31));
