@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+from functools import lru_cache
 from pathlib import Path
 
 import numpy as np
@@ -139,18 +140,36 @@ def call(name: str, *args) -> None:
 # ---- marshalling helpers -------------------------------------------------------
 
 
+# Small index lists go straight into ctypes arrays (no NumPy array + ctypes
+# cast per argument: ~1 us each, which made the per-gate host cost of small
+# states ~15 us of Python against ~6 us in the C library).
 def i32(values) -> tuple:
-    arr = np.ascontiguousarray(np.asarray(list(values), dtype=np.int32))
-    return arr, (arr.ctypes.data_as(_i32p) if arr.size else None)
+    vals = [int(v) for v in values]
+    return vals, ((C.c_int32 * len(vals))(*vals) if vals else None)
+
+
+@lru_cache(maxsize=512)
+def _array_type(ctype, n: int):
+    return ctype * n
 
 
 def i64(values) -> tuple:
-    arr = np.ascontiguousarray(np.asarray(values, dtype=np.int64))
-    return arr, arr.ctypes.data_as(_i64p)
+    arr = np.ascontiguousarray(values, dtype=np.int64)
+    try:
+        return arr, _array_type(C.c_int64, arr.size).from_buffer(arr)
+    except (TypeError, ValueError, BufferError):  # read-only input: fall back to the address
+        return arr, C.cast(C.c_void_p(arr.ctypes.data), _i64p)
 
 
 def ptr(arr: np.ndarray):
-    return C.c_void_p(arr.ctypes.data)
+    """Address of a C-contiguous array for a void* parameter (a ctypes view of
+    the buffer: no copy, ~0.6 us instead of ~2 us for arr.ctypes.data)."""
+    if arr.nbytes == 0:
+        return None
+    try:
+        return _array_type(C.c_char, arr.nbytes).from_buffer(arr)
+    except (TypeError, ValueError, BufferError):  # read-only / foreign buffers
+        return C.c_void_p(arr.ctypes.data)
 
 
 def dtype_code(dtype) -> int:
