@@ -129,7 +129,10 @@ def main():
         20, fusion.fuse(rg, fusion.FusionConfig(5, 6)).gates, np.complex128)
     # ---- config 2: random-30 complex64, unfused
     g2 = random_gate_sequence(30, 200, np.random.default_rng(0), max_arity=2)
-    rows["2_random30_c64"] = {"gpu": gpu_run(30, g2, np.complex64, len(g2))}
+    f2 = fuse_auto(g2, 5)
+    rows["2_random30_c64"] = {"gpu": gpu_run(30, g2, np.complex64, len(g2)),
+                              "gpu_fused_auto5": gpu_run(30, f2.ops, np.complex64, len(g2)),
+                              "fused_windows": f2.data_passes}
     rows["2_random30_c64"]["cpu_reference"] = cpu_ref(26, to_ref(random_gate_sequence(
         26, CPU_GATES, np.random.default_rng(0), max_arity=2)), np.complex64, full_n=30, full_count=200)
     # ---- config 4 per GPU: QV-33 complex128 fold k = 4 (one of the two 2^33 segments of QV-34 on 2 GPUs)
