@@ -827,6 +827,30 @@ int enable_peer(int from, int to) {
   return DSV_OK;
 }
 
+// Small pinned host buffers for deferred reductions (dsv_group_*), kept in a
+// process-wide free list: cudaMallocHost / cudaFreeHost cost milliseconds and
+// synchronise the device, and a sharded state is rebuilt per circuit.
+std::mutex g_pinned_mu;
+std::vector<std::pair<double*, size_t>> g_pinned_free;
+
+bool pinned_take(size_t n, double** out, size_t* out_n) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  for (size_t i = 0; i < g_pinned_free.size(); ++i)
+    if (g_pinned_free[i].second >= n) {
+      *out = g_pinned_free[i].first;
+      *out_n = g_pinned_free[i].second;
+      g_pinned_free.erase(g_pinned_free.begin() + long(i));
+      return true;
+    }
+  return false;
+}
+
+void pinned_put(double* p, size_t n) {
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  if (g_pinned_free.size() < 64) g_pinned_free.push_back({p, n});
+  else cudaFreeHost(p);
+}
+
 // reduce partials already on device -> host doubles
 int finish_reduce(dsv_state* s, uint64_t nbins, uint64_t nchunks, int ncomp, double* d_partial,
                   double* d_out, double* host_out) {
@@ -836,13 +860,15 @@ int finish_reduce(dsv_state* s, uint64_t nbins, uint64_t nchunks, int ncomp, dou
     if (s->pinned_n < n) {
       if (s->pinned) {
         CK(cudaStreamSynchronize(s->stream));
-        CK(cudaFreeHost(s->pinned));
+        pinned_put(s->pinned, s->pinned_n);
         s->pinned = nullptr;
         s->pinned_n = 0;
       }
       const size_t want = std::max<size_t>(n, 512);
-      CK(cudaMallocHost(&s->pinned, sizeof(double) * want));
-      s->pinned_n = want;
+      if (!pinned_take(want, &s->pinned, &s->pinned_n)) {
+        CK(cudaMallocHost(&s->pinned, sizeof(double) * want));
+        s->pinned_n = want;
+      }
     }
     CK(cudaMemcpyAsync(s->pinned, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
     s->pending_n = n;
@@ -1059,7 +1085,7 @@ int dsv_state_destroy(dsv_state* s) {
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   for (auto e : s->uev)
     if (e) cudaEventDestroy(e);
-  if (s->pinned) cudaFreeHost(s->pinned);
+  if (s->pinned) pinned_put(s->pinned, s->pinned_n);  // reused by the next state (cudaFreeHost synchronises)
   if (s->d && s->owned && !s->ipc && !s->exported && g_pool_env) {
     pool_put({s->device, amp_bytes(s->dtype) << s->nbits, s->d, s->stream, s->scratch, s->scratch_bytes, s->gdata,
               s->gdata_bytes});

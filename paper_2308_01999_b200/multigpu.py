@@ -16,8 +16,10 @@ GPU, distsim.py:69-277, made multi-process).
   single-process engine (one host thread, all GPUs) is shard.py; this module
   is the torchrun (one process per GPU) form.
 * Reductions (norm, marginals, Pauli expectations) reduce per rank on the
-  GPU and all-reduce a handful of float64s through torch.distributed (NCCL
-  on a GPU job, gloo on CPU tests).
+  GPU and all-reduce a handful of float64s over the control plane: by
+  default the PyTorch-free SocketComm (comm.py, TCP star around rank 0,
+  rank-order sums); TorchComm (torch.distributed, NCCL / gloo) plugs in the
+  same way.
 
 The segment backend is pluggable so the host protocol (planning, roles,
 predicates, reductions) is tested on CPU with world_size=2 gloo and a NumPy
@@ -168,7 +170,11 @@ class DistributedStateVector:
     """2^n amplitudes over `world` processes (world = 2^g), one segment each."""
 
     def __init__(self, num_qubits: int, dtype=np.complex64, comm=None, segment_factory=None):
-        self.comm = comm if comm is not None else TorchComm()
+        if comm is None:
+            from .comm import SocketComm
+
+            comm = SocketComm()
+        self.comm = comm
         world = self.comm.world
         g = int(round(math.log2(world)))
         if 1 << g != world:
@@ -323,30 +329,20 @@ class DistributedStateVector:
         return phys[src]
 
 
-# ---- benchmark leg (bench.py --gpus N under torchrun) -------------------------------------------
+# ---- benchmark leg (bench.py --gpus N under torchrun, DSV_BENCH_MULTIPROC=1) -----------------
 
 def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler, peaks, cpu_cores):
+    """One process per GPU, PyTorch-free: SocketComm control plane, CUDA IPC
+    data plane, device time max over ranks (bench.py contract)."""
     import json
     import time
 
-    import torch
-    import torch.distributed as dist
-
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    ndev = max(1, torch.cuda.device_count())
-    local_dev = local % ndev  # >1 rank per GPU only for functional runs on a 1-GPU box
-    torch.cuda.set_device(local_dev)
-    # NCCL for the scalar reductions; DSV_DIST_BACKEND=gloo allows several ranks per GPU
-    backend = os.environ.get("DSV_DIST_BACKEND", "nccl")
-    if not dist.is_initialized():
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_dev}"))
-        else:
-            dist.init_process_group(backend)
-    comm = TorchComm()
-    comm.local_rank = local_dev
     from . import _native as N
+    from .comm import SocketComm
 
+    comm = SocketComm()
+    ndev = max(1, N.device_count())
+    local_dev = comm.local_rank % ndev  # > 1 rank per GPU only for functional runs on a 1-GPU box
     gates, ops, fuse_s = workload(getattr(args, "fusion", "fold"))
     dsv = DistributedStateVector(n_qubits, np.complex64, comm)
     seg = dsv.seg.seg
@@ -364,7 +360,6 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
     clocks = ClockSampler(local_dev).start()
     launches0 = N.launch_count()
     comm.barrier()
-    torch.cuda.synchronize()
     t0 = time.perf_counter()
     seg.event_record(0)
     for _ in range(args.steps):
@@ -403,7 +398,7 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
     gate_bytes = sum(int(getattr(g, "matrix", np.zeros(0)).size) * 8 for g in ops)
     if comm.rank == 0:
         pk = peaks()
-        dom_name, dom_v = max(prof.items(), key=lambda kv: kv[1]["ms"])
+        dom_name, dom_v = max(((k, v) for k, v in prof.items() if k != "exchange"), key=lambda kv: kv[1]["ms"])
         achieved = dom_v["bytes"] / (dom_v["ms"] / 1000.0) / 1e9
         line = {
             "metric": metric, "value": value, "unit": "gates/s", "n_gpus": comm.world, "steps": args.steps,
@@ -412,8 +407,9 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
             "data": "synthetic (QFT-33 circuit generated on the host, state starts at |0>)",
             "config": {"workload": "qft33_c64_fused_k5", "n_qubits": n_qubits, "circuit_gates": len(gates),
                        "fused_ops": len(ops), "fusion": getattr(args, "fusion", "fold"),
-                       "global_bits": dsv.global_bits,
-                       "l2": "segment >= 8 GiB >> 126 MB L2", "parallelism": f"sv-shard{comm.world} (P2P NVLink swaps)"},
+                       "global_bits": dsv.global_bits, "l2": "segment >= 8 GiB >> 126 MB L2",
+                       "parallelism": f"sv-shard{comm.world}: one process per GPU (SocketComm control plane, "
+                                      "CUDA IPC masked exchanges over NVLink)"},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None},
             "transfer_stats": dsv.stats.as_dict(),
@@ -427,4 +423,4 @@ def bench_main(args, metric, n_qubits, fusion, published, workload, ClockSampler
         }
         print(json.dumps(line), flush=True)
     comm.barrier()
-    dist.destroy_process_group()
+    comm.close()

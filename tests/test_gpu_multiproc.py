@@ -1,16 +1,16 @@
 """The real multi-process segment backend (CUDA IPC mappings + the in-place
 exchange kernel) with two and four processes.  On a one-GPU box all ranks
 share cuda:0 — the IPC/exchange code path is identical to the NVLink case,
-only the peer memory is local.  Control plane over gloo (NCCL refuses two
-ranks on one GPU)."""
+only the peer memory is local.  Control plane: the PyTorch-free SocketComm
+(comm.py) that multigpu.py uses by default."""
 
 import os
 import socket
 
+import multiprocessing as mp
+
 import numpy as np
 import pytest
-import torch.distributed as dist
-import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
@@ -23,17 +23,18 @@ def _free_port():
 
 def _worker(rank, world, port, q, dtype_name):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
-                      LOCAL_RANK=str(rank))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+                      LOCAL_RANK=str(rank), DSV_COMM_PORT=str(port))
+    comm = None
     try:
         from oracle import sv_oracle as O
         from paper_2308_01999_b200 import gates as G
         from paper_2308_01999_b200.circuits import gen_qft, random_gate_sequence, to_gates
         from paper_2308_01999_b200.fusion import FusionConfig, fuse
-        from paper_2308_01999_b200.multigpu import DistributedStateVector, TorchComm
+        from paper_2308_01999_b200.comm import SocketComm
+        from paper_2308_01999_b200.multigpu import DistributedStateVector
 
         dtype = np.dtype(dtype_name)
-        comm = TorchComm()
+        comm = SocketComm()
         n = 12
         rng = np.random.default_rng(5)
         gates = fuse(to_gates(gen_qft(n)), FusionConfig(4, 6)).gates
@@ -55,7 +56,8 @@ def _worker(rank, world, port, q, dtype_name):
         q.put({"error": repr(e)})
         raise
     finally:
-        dist.destroy_process_group()
+        if comm is not None:
+            comm.close()
 
 
 @pytest.mark.parametrize("world,dtype", [(2, "complex128"), (4, "complex64")])

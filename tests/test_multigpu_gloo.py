@@ -1,5 +1,6 @@
 """The one-process-per-GPU layer (paper_2308_01999_b200/multigpu.py) on CPU:
-world_size 2 and 4 over gloo, with a NumPy segment double standing in for
+world_size 2 and 4 over gloo (TorchComm) and over the PyTorch-free socket
+control plane (comm.SocketComm), with a NumPy segment double standing in for
 the libdsv/NVLink segment.  Exercises the real host protocol — relocation
 planning, partner roles, global-control predicates, the exchange sequence,
 reductions and transfer accounting — and checks the gathered state against
@@ -100,6 +101,9 @@ class NumpySegment:
         pass
 
     def _sendrecv(self, partner, payload, low):
+        if getattr(self.comm, "backend", "") == "socket":  # every rank is in one pair per round
+            parts = self.comm.all_gather_bytes(np.ascontiguousarray(payload).tobytes())
+            return np.frombuffer(parts[partner], dtype=np.complex128).copy()
         import torch
 
         out = torch.from_numpy(np.ascontiguousarray(payload).view(np.float64).copy())
@@ -120,6 +124,8 @@ class NumpySegment:
 
     def exchange_all(self, partner, i_am_low):
         if partner == self.comm.rank:
+            if getattr(self.comm, "backend", "") == "socket":
+                self.comm.all_gather_bytes(b"")  # stay in step with the pairs that do exchange
             return
         self.a = self._sendrecv(partner, self.a.astype(np.complex128), self.comm.rank < partner).astype(self.dtype)
 
@@ -130,17 +136,23 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, kind="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK=str(rank))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if kind == "gloo":
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import sv_oracle as O
         from paper_2308_01999_b200 import gates as G
         from paper_2308_01999_b200.circuits import gen_qft, random_gate_sequence, to_gates
         from paper_2308_01999_b200.multigpu import DistributedStateVector, TorchComm
 
-        comm = TorchComm()
+        if kind == "gloo":
+            comm = TorchComm()
+        else:  # the PyTorch-free control plane (comm.py)
+            from paper_2308_01999_b200.comm import SocketComm
+
+            comm = SocketComm(rank, world, "127.0.0.1", port)
         n = 7
         rng = np.random.default_rng(11)
         gates = to_gates(gen_qft(n)) + random_gate_sequence(n, 25, rng, max_arity=2)
@@ -180,15 +192,17 @@ def _worker(rank, world, port, q):
         q.put({"error": repr(e)})
         raise
     finally:
-        dist.destroy_process_group()
+        if kind == "gloo":
+            dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("kind", ["gloo", "socket"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_distributed_protocol_over_gloo(world):
+def test_distributed_protocol_over_gloo(world, kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, kind)) for r in range(world)]
     for p in procs:
         p.start()
     fold = q.get(timeout=240)
