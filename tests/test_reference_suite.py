@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.skipif(not (SUITE / "SHA256SUMS").exists(), reason="reference suite not staged (tools/ref_suite.sh stage)")
 def test_reference_hot_path_suite_passes_against_the_drop_in(gpu_available):
-    res = subprocess.run(["bash", str(ROOT / "tools" / "ref_suite.sh"), "run", "-q"], capture_output=True, text=True,
+    res = subprocess.run(["bash", str(ROOT / "tools" / "ref_suite.sh"), "run"], capture_output=True, text=True,
                          timeout=900)
     tail = (res.stdout + res.stderr)[-3000:]
     assert res.returncode == 0, tail
