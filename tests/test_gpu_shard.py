@@ -181,3 +181,20 @@ def test_sharded_equals_single_segment_statevector():
         single.apply(g)
     got, _ = _run(n, 4, gates, np.complex64)
     assert np.abs(got - single.logical_amplitudes()).max() <= 1e-5
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_fold_and_cluster_fused_c128_sharded(P):
+    """complex128 sharded runs of both opt-in fusers' ops (phased windows with
+    global outside qubits folded per segment; cluster-fused dense windows)."""
+    from paper_2308_01999_b200.fusion_cluster import fuse_cluster
+    from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+    n = 16
+    for ops, want in ((fuse_fold(to_gates(gen_qft(n)), 5).ops, O.run_circuit(to_gates(gen_qft(n)), n)),
+                      (fuse_cluster(to_gates(gen_qv(n, 8, seed=3)), 4).ops,
+                       O.run_circuit(to_gates(gen_qv(n, 8, seed=3)), n))):
+        sv = ShardedStateVector(n, [0] * P, np.complex128)
+        sv.run(ops)
+        assert np.abs(sv.gather_logical() - want).max() <= 1e-12
+        sv.close()
