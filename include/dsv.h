@@ -198,6 +198,21 @@ int dsv_ipc_handle(dsv_state* s, void* out64);
  * handle owned by device `device` (the mapping is closed on destroy) */
 int dsv_peer_open(int device, int nbits, int dtype, const void* handle64, dsv_state** out);
 
+/* ---- CUDA graphs: record the device work of a gate sequence, replay it ---- */
+/* Between dsv_capture_begin and dsv_capture_end the gate entry points of `s`
+ * (apply_matrix / genperm / matrix_phased / pauli rotation and product /
+ * swap_index_bits / set_basis / set_zero / scale) are recorded on the state's
+ * stream instead of executed; per-gate tables are baked into buffers owned by
+ * the graph.  Reductions, host transfers and exchanges return DSV_EINVAL while
+ * capturing.  dsv_graph_launch replays the recorded work on the same state
+ * (one launch for the whole sequence: the small-state circuits the host's
+ * per-gate call overhead dominates). */
+typedef struct dsv_graph dsv_graph;
+int dsv_capture_begin(dsv_state* s);
+int dsv_capture_end(dsv_state* s, dsv_graph** out);
+int dsv_graph_launch(dsv_graph* g, dsv_state* s);
+int dsv_graph_destroy(dsv_graph* g);
+
 /* ---- instrumentation (bench.py) ----------------------------------------- */
 /* When enabled, every kernel launched on `s` is bracketed by CUDA events on
  * the state's stream and tagged with its kernel class and algorithmic bytes

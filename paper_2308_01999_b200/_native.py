@@ -80,6 +80,10 @@ SIGNATURES: dict[str, list] = {
     "dsv_group_expect_pauli": [C.POINTER(_vp), _int, _i32p, C.c_char_p, _int, _dp],
     "dsv_ipc_handle": [_vp, _vp],
     "dsv_peer_open": [_int, _int, _int, _vp, C.POINTER(_vp)],
+    "dsv_capture_begin": [_vp],
+    "dsv_capture_end": [_vp, C.POINTER(_vp)],
+    "dsv_graph_launch": [_vp, _vp],
+    "dsv_graph_destroy": [_vp],
     "dsv_prof_enable": [_vp, _int],
     "dsv_prof_reset": [_vp],
     "dsv_prof_read": [_vp, _u64p, _dp, _dp],
@@ -419,6 +423,15 @@ class NativeState:
         call("dsv_ipc_handle", self._h, buf)
         return buf.raw
 
+    # -- CUDA graphs ------------------------------------------------------------------
+    def capture_begin(self) -> None:
+        call("dsv_capture_begin", self._h)
+
+    def capture_end(self) -> "Graph":
+        out = _vp()
+        call("dsv_capture_end", self._h, C.byref(out))
+        return Graph(out.value, self)
+
     # -- instrumentation ------------------------------------------------------------
     def prof_enable(self, on: bool = True) -> None:
         call("dsv_prof_enable", self._h, 1 if on else 0)
@@ -477,3 +490,25 @@ def group_expect_pauli(states, factors) -> np.ndarray:
     out = np.zeros((len(states), 2), dtype=np.float64)
     call("dsv_group_expect_pauli", _handles(states), len(states), bp, ps, len(bits), out.ctypes.data_as(_dp))
     return out[:, 0] + 1j * out[:, 1]
+
+
+class Graph:
+    """A recorded gate sequence of one NativeState (dsv_capture_* / dsv_graph_*)."""
+
+    def __init__(self, handle, state: NativeState):
+        self._h = handle
+        self._state = state  # keeps the state (whose pointers the graph holds) alive
+
+    def launch(self) -> None:
+        call("dsv_graph_launch", self._h, self._state._h)
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None:
+            lib().dsv_graph_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass

@@ -206,6 +206,14 @@ struct dsv_state {
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t uev[16] = {};
+  // CUDA-graph capture (dsv_capture_begin/end): per-gate tables go to
+  // buffers owned by the graph, filled at capture time
+  bool capturing = false;
+  std::vector<void*> cap_bufs;
+  void* keep_gdata = nullptr;
+  size_t keep_gdata_bytes = 0;
+  void* keep_scratch = nullptr;
+  size_t keep_scratch_bytes = 0;
   // deferred reductions (dsv_group_*): results land in pinned host memory and
   // the call returns before the GPU finishes
   bool defer = false;
@@ -219,7 +227,20 @@ namespace {
 size_t amp_bytes(int dtype) { return dtype == DSV_C128 ? 16 : 8; }
 uint64_t namps(const dsv_state* s) { return 1ull << s->nbits; }
 
+// while capturing a graph every table gets its own buffer (the graph replays
+// them later; the stream-ordered reuse of one buffer would alias them)
+int capture_buffer(dsv_state* s, size_t bytes, void** out, size_t* out_bytes) {
+  const size_t want = std::max<size_t>(bytes, 256);
+  void* p = nullptr;
+  CK(cudaMalloc(&p, want));
+  s->cap_bufs.push_back(p);
+  *out = p;
+  *out_bytes = want;
+  return DSV_OK;
+}
+
 int ensure_scratch(dsv_state* s, size_t bytes) {
+  if (s->capturing) return capture_buffer(s, bytes, &s->scratch, &s->scratch_bytes);
   if (s->scratch_bytes >= bytes) return DSV_OK;
   if (s->scratch) {
     CK(cudaStreamSynchronize(s->stream));
@@ -234,6 +255,7 @@ int ensure_scratch(dsv_state* s, size_t bytes) {
 }
 
 int ensure_gdata(dsv_state* s, size_t bytes) {
+  if (s->capturing) return capture_buffer(s, bytes, &s->gdata, &s->gdata_bytes);
   if (s->gdata_bytes >= bytes) return DSV_OK;
   if (s->gdata) {
     CK(cudaStreamSynchronize(s->stream));
@@ -244,6 +266,19 @@ int ensure_gdata(dsv_state* s, size_t bytes) {
   size_t want = std::max<size_t>(bytes, size_t(64) << 10);
   CK(cudaMalloc(&s->gdata, want));
   s->gdata_bytes = want;
+  return DSV_OK;
+}
+
+// per-gate table upload: stream-ordered normally; baked synchronously into the
+// graph-owned buffer while capturing (a captured memcpy would read the host
+// temporary again at every replay)
+cudaError_t h2d(dsv_state* s, void* dst, const void* src, size_t bytes) {
+  if (s->capturing) return cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s->stream);
+}
+
+int no_capture(const dsv_state* s, const char* what) {
+  if (s && s->capturing) return fail(DSV_EINVAL, "%s is not allowed while a graph is being captured", what);
   return DSV_OK;
 }
 
@@ -264,7 +299,7 @@ struct ProfTok {
 
 ProfTok prof_start(dsv_state* s) {
   ProfTok t;
-  if (s->prof_on) {
+  if (s->prof_on && !s->capturing) {
     t.a = pool_event(s);
     cudaEventRecord(t.a, s->stream);
   }
@@ -272,7 +307,7 @@ ProfTok prof_start(dsv_state* s) {
 }
 
 void prof_stop(dsv_state* s, ProfTok t, int cls, double bytes) {
-  if (!s->prof_on || !t.a) return;
+  if (!s->prof_on || !t.a || s->capturing) return;
   cudaEvent_t b = pool_event(s);
   cudaEventRecord(b, s->stream);
   s->recs.push_back(ProfRec{cls, t.a, b, bytes});
@@ -683,7 +718,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     }
     if (!rvec.empty()) std::memcpy(host.data() + bbytes + tbytes, rvec.data(), rvec.size() * sizeof(float));
     if (int rc = ensure_gdata(s, host.size())) return rc;
-    CK(cudaMemcpyAsync(s->gdata, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+    CK(h2d(s, s->gdata, host.data(), host.size()));
     const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
     d.htab = reinterpret_cast<const float*>(host.data() + bbytes);
     d.d_rvec = rvec.empty() ? nullptr : d_b + bbytes + tbytes;
@@ -735,7 +770,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     std::memcpy(host.data() + limb_bytes + i * 4, &f, 4);
   }
   if (int rc = ensure_gdata(s, host.size())) return rc;
-  CK(cudaMemcpyAsync(s->gdata, host.data(), host.size(), cudaMemcpyHostToDevice, s->stream));
+  CK(h2d(s, s->gdata, host.data(), host.size()));
   const unsigned char* d_b = static_cast<const unsigned char*>(s->gdata);
   d.htab = reinterpret_cast<const float*>(host.data() + limb_bytes);
   ProfTok t = prof_start(s);
@@ -783,7 +818,7 @@ int apply_low(dsv_state* s, const GateGeom& gg, const void* matrix, const std::v
     std::vector<float> host(tab.size());
     for (size_t i = 0; i < tab.size(); ++i) host[i] = float(tab[i]);
     if (int rc = ensure_gdata(s, host.size() * sizeof(float))) return rc;
-    CK(cudaMemcpyAsync(s->gdata, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+    CK(h2d(s, s->gdata, host.data(), host.size() * sizeof(float)));
   }
   std::vector<cplx<float>> m;
   canon_matrix<float>(gg, matrix, m);
@@ -1118,6 +1153,7 @@ int dsv_state_device_ptr(const dsv_state* s, void** out) {
 }
 
 int dsv_sync(dsv_state* s) {
+  if (int rc = no_capture(s, "dsv_sync")) return rc;
   if (int rc = check_state(s)) return rc;
   DeviceGuard g(s->device);
   CK(cudaStreamSynchronize(s->stream));
@@ -1147,6 +1183,7 @@ int dsv_set_basis(dsv_state* s, uint64_t index) {
 }
 
 int dsv_upload(dsv_state* s, uint64_t begin, uint64_t count, const void* host) {
+  if (int rc = no_capture(s, "dsv_upload")) return rc;
   if (int rc = check_state(s)) return rc;
   if (begin > namps(s) || count > namps(s) - begin) return fail(DSV_EINVAL, "upload range exceeds state");
   if (count == 0) return DSV_OK;
@@ -1158,6 +1195,7 @@ int dsv_upload(dsv_state* s, uint64_t begin, uint64_t count, const void* host) {
 }
 
 int dsv_download(dsv_state* s, uint64_t begin, uint64_t count, void* host) {
+  if (int rc = no_capture(s, "dsv_download")) return rc;
   if (int rc = check_state(s)) return rc;
   if (begin > namps(s) || count > namps(s) - begin) return fail(DSV_EINVAL, "download range exceeds state");
   if (count == 0) return DSV_OK;
@@ -1169,6 +1207,8 @@ int dsv_download(dsv_state* s, uint64_t begin, uint64_t count, void* host) {
 }
 
 int dsv_copy(dsv_state* dst, const dsv_state* src) {
+  if (int rc = no_capture(dst, "dsv_copy")) return rc;
+  if (int rc = no_capture(src, "dsv_copy")) return rc;
   if (int rc = check_state(dst)) return rc;
   if (int rc = check_state(src)) return rc;
   if (dst->nbits != src->nbits || dst->dtype != src->dtype) return fail(DSV_EINVAL, "copy between states of different shape");
@@ -1359,13 +1399,13 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   char* base = static_cast<char*>(s->scratch);
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(base);
   void* d_mt = base + ((off_bytes + 255) / 256) * 256;
-  CK(cudaMemcpyAsync(d_offs, uv.offs.data(), off_bytes, cudaMemcpyHostToDevice, s->stream));
-  CK(cudaMemcpyAsync(d_mt, mt.data(), mat_bytes, cudaMemcpyHostToDevice, s->stream));
+  CK(h2d(s, d_offs, uv.offs.data(), off_bytes));
+  CK(h2d(s, d_mt, mt.data(), mat_bytes));
   ProfTok t = prof_start(s);
   CKL(launch_dense_generic(s->dtype, k, uv.g, d_offs, d_mt, s->d, s->stream), 1);
   prof_stop(s, t, PC_DENSE_GENERIC, bytes);
   // the host staging vectors die at return: make the copies complete first
-  CK(cudaStreamSynchronize(s->stream));
+  if (!s->capturing) CK(cudaStreamSynchronize(s->stream));
   return DSV_OK;
 }
 
@@ -1447,7 +1487,7 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
     }
   }
   if (int rc = ensure_gdata(s, raw.size())) return rc;
-  CK(cudaMemcpyAsync(s->gdata, raw.data(), raw.size(), cudaMemcpyHostToDevice, s->stream));
+  CK(h2d(s, s->gdata, raw.data(), raw.size()));
   const double bytes = 2.0 * double(amp_bytes(s->dtype)) * double(namps(s));
   ProfTok t = prof_start(s);
   bool lowbits = k <= 4;
@@ -1620,7 +1660,7 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
       if (touched) fl[x] |= 2;
     }
     if (int rc = ensure_gdata(s, tab.size())) return rc;
-    CK(cudaMemcpyAsync(s->gdata, tab.data(), tab.size(), cudaMemcpyHostToDevice, s->stream));
+    CK(h2d(s, s->gdata, tab.data(), tab.size()));
     ProfTok t = prof_start(s);
     CKL(launch_diag_stream(s->dtype, s->nbits, kk, B.data(), s->gdata, s->d, s->stream), 1);
     prof_stop(s, t, PC_DIAG, bytes);
@@ -1713,14 +1753,14 @@ int dsv_apply_genperm(dsv_state* s, const int64_t* perm, const void* diag, const
   const size_t obr = ((ob + 255) / 256) * 256;
   if (int rc = ensure_scratch(s, 2 * obr + dn.size() + 256)) return rc;
   char* base = static_cast<char*>(s->scratch);
-  CK(cudaMemcpyAsync(base, uv.offs.data(), ob, cudaMemcpyHostToDevice, s->stream));
-  CK(cudaMemcpyAsync(base + obr, oo.data(), ob, cudaMemcpyHostToDevice, s->stream));
-  CK(cudaMemcpyAsync(base + 2 * obr, dn.data(), dn.size(), cudaMemcpyHostToDevice, s->stream));
+  CK(h2d(s, base, uv.offs.data(), ob));
+  CK(h2d(s, base + obr, oo.data(), ob));
+  CK(h2d(s, base + 2 * obr, dn.data(), dn.size()));
   ProfTok t = prof_start(s);
   CKL(launch_perm_generic(s->dtype, k, uv.g, reinterpret_cast<uint64_t*>(base),
                           reinterpret_cast<uint64_t*>(base + obr), base + 2 * obr, s->d, s->stream), 1);
   prof_stop(s, t, PC_PERM_GENERIC, bytes);
-  CK(cudaStreamSynchronize(s->stream));
+  if (!s->capturing) CK(cudaStreamSynchronize(s->stream));
   return DSV_OK;
 }
 
@@ -1859,6 +1899,7 @@ static int check_ordering(const dsv_state* s, const int32_t* ordering) {
 static const uint64_t kAccessChunk = 1ull << 25;
 
 int dsv_access_get(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64_t end, void* host_out) {
+  if (int rc = no_capture(s, "dsv_access_get")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (int rc = check_ordering(s, ordering)) return rc;
@@ -1881,6 +1922,7 @@ int dsv_access_get(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64
 }
 
 int dsv_access_set(dsv_state* s, const int32_t* ordering, uint64_t begin, uint64_t count, const void* host_in) {
+  if (int rc = no_capture(s, "dsv_access_set")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (int rc = check_ordering(s, ordering)) return rc;
@@ -2008,6 +2050,7 @@ static int probs_impl(dsv_state* s, const int32_t* bits, int k, bool allow_vec2,
 }
 
 int dsv_norm2(dsv_state* s, double* out) {
+  if (int rc = no_capture(s, "dsv_norm2")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   DeviceGuard g(s->device);
@@ -2015,6 +2058,7 @@ int dsv_norm2(dsv_state* s, double* out) {
 }
 
 int dsv_marginal_probs(dsv_state* s, const int32_t* bits, int k, double* out) {
+  if (int rc = no_capture(s, "dsv_marginal_probs")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   DeviceGuard g(s->device);
@@ -2022,6 +2066,7 @@ int dsv_marginal_probs(dsv_state* s, const int32_t* bits, int k, double* out) {
 }
 
 int dsv_expect_pauli(dsv_state* s, const int32_t* bits, const char* paulis, int m, double* out) {
+  if (int rc = no_capture(s, "dsv_expect_pauli")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   PauliMasks pm;
@@ -2047,6 +2092,8 @@ int dsv_expect_pauli(dsv_state* s, const int32_t* bits, const char* paulis, int 
 }
 
 int dsv_inner(dsv_state* a, const dsv_state* b, double* out) {
+  if (int rc = no_capture(a, "dsv_inner")) return rc;
+  if (int rc = no_capture(b, "dsv_inner")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(a)) return rc;
   if (int rc = check_state(b)) return rc;
@@ -2068,6 +2115,7 @@ int dsv_inner(dsv_state* a, const dsv_state* b, double* out) {
 }
 
 int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, int k, double* out) {
+  if (int rc = no_capture(s, "dsv_expect_matrix")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!matrix) return fail(DSV_EINVAL, "null matrix");
@@ -2110,6 +2158,7 @@ int dsv_expect_matrix(dsv_state* s, const void* matrix, const int32_t* targets, 
 }
 
 int dsv_collapse(dsv_state* s, const int32_t* bits, int k, uint64_t outcome, double norm2_kept) {
+  if (int rc = no_capture(s, "dsv_collapse")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (!(norm2_kept > 0.0)) return fail(DSV_EINVAL, "collapse onto a zero-probability outcome");
@@ -2143,6 +2192,7 @@ int dsv_scale(dsv_state* s, double factor) {
 }
 
 int dsv_sample(dsv_state* s, const double* variates, int64_t shots, uint64_t* outcomes) {
+  if (int rc = no_capture(s, "dsv_sample")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(s)) return rc;
   if (shots < 1) return fail(DSV_EINVAL, "shots must be >= 1");
@@ -2194,6 +2244,8 @@ int dsv_sample(dsv_state* s, const double* variates, int64_t shots, uint64_t* ou
 // ---- segments -----------------------------------------------------------------------------
 
 int dsv_exchange_halves(dsv_state* a, dsv_state* b, int local_bit, int part, int nparts) {
+  if (int rc = no_capture(a, "dsv_exchange_halves")) return rc;
+  if (int rc = no_capture(b, "dsv_exchange_halves")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(a)) return rc;
   if (int rc = check_state(b)) return rc;
@@ -2219,6 +2271,8 @@ int dsv_exchange_halves(dsv_state* a, dsv_state* b, int local_bit, int part, int
 }
 
 int dsv_exchange_all(dsv_state* a, dsv_state* b) {
+  if (int rc = no_capture(a, "dsv_exchange_all")) return rc;
+  if (int rc = no_capture(b, "dsv_exchange_all")) return rc;
   DSV_NVTX_RANGE();
   if (int rc = check_state(a)) return rc;
   if (int rc = check_state(b)) return rc;
@@ -2297,6 +2351,8 @@ int run_masked(dsv_state* run, dsv_state* a, dsv_state* b, const MaskedPlan& mp,
 
 int dsv_exchange_masked(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b,
                         int part, int nparts) {
+  if (int rc = no_capture(a, "dsv_exchange_masked")) return rc;
+  if (int rc = no_capture(b, "dsv_exchange_masked")) return rc;
   DSV_NVTX_RANGE();
   MaskedPlan mp;
   if (int rc = plan_masked(a, b, lbits, q, pat_a, pat_b, &mp)) return rc;
@@ -2313,6 +2369,8 @@ int dsv_exchange_masked(dsv_state* a, dsv_state* b, const int32_t* lbits, int q,
 }
 
 int dsv_exchange_pair(dsv_state* a, dsv_state* b, const int32_t* lbits, int q, uint64_t pat_a, uint64_t pat_b) {
+  if (int rc = no_capture(a, "dsv_exchange_pair")) return rc;
+  if (int rc = no_capture(b, "dsv_exchange_pair")) return rc;
   DSV_NVTX_RANGE();
   MaskedPlan mp;
   if (int rc = plan_masked(a, b, lbits, q, pat_a, pat_b, &mp)) return rc;
@@ -2403,6 +2461,87 @@ int dsv_group_marginal_probs(dsv_state** s, int count, const int32_t* bits, int 
 
 int dsv_group_expect_pauli(dsv_state** s, int count, const int32_t* bits, const char* paulis, int m, double* out) {
   return group_reduce(s, count, 2, out, [&](dsv_state* st) { return dsv_expect_pauli(st, bits, paulis, m, nullptr); });
+}
+
+// ---- CUDA graphs: record a gate sequence once, replay it -------------------------------------
+
+struct dsv_graph {
+  dsv_state* state = nullptr;
+  int device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void*> bufs;  // per-gate tables baked at capture time
+};
+
+int dsv_capture_begin(dsv_state* s) {
+  if (int rc = check_state(s)) return rc;
+  if (s->capturing) return fail(DSV_EINVAL, "already capturing");
+  if (s->ipc) return fail(DSV_EINVAL, "cannot capture on a peer mapping");
+  DeviceGuard g(s->device);
+  s->keep_gdata = s->gdata;
+  s->keep_gdata_bytes = s->gdata_bytes;
+  s->keep_scratch = s->scratch;
+  s->keep_scratch_bytes = s->scratch_bytes;
+  s->cap_bufs.clear();
+  CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed));
+  s->capturing = true;
+  return DSV_OK;
+}
+
+static void capture_restore(dsv_state* s) {
+  s->capturing = false;
+  s->gdata = s->keep_gdata;
+  s->gdata_bytes = s->keep_gdata_bytes;
+  s->scratch = s->keep_scratch;
+  s->scratch_bytes = s->keep_scratch_bytes;
+}
+
+int dsv_capture_end(dsv_state* s, dsv_graph** out) {
+  if (int rc = check_state(s)) return rc;
+  if (!out) return fail(DSV_EINVAL, "null argument");
+  *out = nullptr;
+  if (!s->capturing) return fail(DSV_EINVAL, "not capturing");
+  DeviceGuard g(s->device);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(s->stream, &graph);
+  capture_restore(s);
+  dsv_graph* gr = new dsv_graph;
+  gr->state = s;
+  gr->device = s->device;
+  gr->bufs.swap(s->cap_bufs);
+  if (e != cudaSuccess) {
+    dsv_graph_destroy(gr);
+    return cuda_fail(e, "cudaStreamEndCapture");
+  }
+  gr->graph = graph;
+  const cudaError_t e2 = cudaGraphInstantiate(&gr->exec, graph, 0);
+  if (e2 != cudaSuccess) {
+    dsv_graph_destroy(gr);
+    return cuda_fail(e2, "cudaGraphInstantiate");
+  }
+  *out = gr;
+  return DSV_OK;
+}
+
+int dsv_graph_launch(dsv_graph* g, dsv_state* s) {
+  if (!g || !g->exec) return fail(DSV_EINVAL, "null graph");
+  if (int rc = check_state(s)) return rc;
+  if (g->state != s) return fail(DSV_EINVAL, "a graph replays on the state it was captured on");
+  if (int rc = no_capture(s, "dsv_graph_launch")) return rc;
+  DeviceGuard dg(s->device);
+  CKL(cudaGraphLaunch(g->exec, s->stream), 1);
+  return DSV_OK;
+}
+
+int dsv_graph_destroy(dsv_graph* g) {
+  if (!g) return DSV_OK;
+  DeviceGuard dg(g->device);
+  cudaDeviceSynchronize();  // a replay may still be reading the baked tables
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  for (void* p : g->bufs) cudaFree(p);
+  delete g;
+  return DSV_OK;
 }
 
 int dsv_ipc_handle(dsv_state* s, void* out64) {

@@ -69,6 +69,30 @@ def gpu_run(n, ops, dtype, gates_count, reps=2):
     return out
 
 
+def gpu_graph_run(n, ops, dtype, gates_count, reps=20):
+    """The same gate sequence recorded once into a CUDA graph
+    (StateVector.capture) and replayed: one launch per pass instead of one
+    host call per gate — what a small state (config 1) is bound by."""
+    sv = StateVector(n, dtype=dtype)
+    nat = sv.native
+    with sv.capture() as rec:
+        for g in ops:
+            sv.apply(g)
+    times = []
+    for _ in range(reps):
+        nat.set_basis(0)
+        sv.bit_map = list(rec.start_map)
+        nat.sync()
+        nat.event_record(0)
+        rec.replay()
+        nat.event_record(1)
+        times.append(nat.event_elapsed(0, 1))
+    rec.close()
+    ms = float(np.median(times))
+    return {"ms_median": ms, "ms_min": min(times), "gates_per_s": gates_count / (ms / 1e3),
+            "launch": "one CUDA graph per pass (StateVector.capture / Recording.replay)"}
+
+
 def cpu_ref(n, gates, dtype, full_n=None, full_count=None):
     api = bench._reference_api()
     assert api is not None, "install the reference first: tools/install_reference.sh"
@@ -121,7 +145,12 @@ def main():
     rows["1_qft20_c128"] = {
         "gpu_unfused": gpu_run(20, g1, np.complex128, len(g1), reps=5),
         "gpu_fused_5_6": gpu_run(20, f1, np.complex128, len(g1), reps=5),
+        "gpu_unfused_graph": gpu_graph_run(20, g1, np.complex128, len(g1)),
+        "gpu_fused_5_6_graph": gpu_graph_run(20, f1, np.complex128, len(g1)),
     }
+    if os.environ.get("CONFIGS_ONLY") == "1":
+        print(json.dumps(rows, indent=1))
+        return
     statevec, fusion, circuits = bench._reference_api()
     rg = ref_gates("qft", 20)
     rows["1_qft20_c128"]["cpu_reference_unfused"] = cpu_ref(20, rg, np.complex128)
