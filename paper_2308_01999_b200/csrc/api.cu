@@ -63,8 +63,13 @@ bool g_tc8ws_env = [] {
 }();
 bool g_tc8ws_all = false;  // A/B: the warp-specialised pipeline for every plain tc8 window
 bool g_tc8ws_row2 = true;
-bool g_tc4_all = false;
-bool g_wt4 = false;  // A/B: complex64 k = 4 gates inside bits 0..5 on the warp-transpose kernel  // A/B: every complex64 k = 4 dense gate on the tensor cores  // A/B: ... for windows with index bit 0 the lowest target
+
+// complex128 k = 5 windows on the tensor cores through 8-bit digits at
+// fp64-level accuracy (tc8d.cu); DSV_TC8D=0 keeps the FP64 CUDA-core kernels.
+bool g_tc8d_env = [] {
+  const char* e = std::getenv("DSV_TC8D");
+  return !(e && e[0] == '0');
+}();
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -561,6 +566,62 @@ bool build_tile_tmap(const dsv_state* s, const GateGeom& gg, TcDesc* d) {
   return r == CUDA_SUCCESS;
 }
 
+// complex128 k = 5 dense window on the tensor cores (tc8d.cu)
+bool tc8d_eligible(const dsv_state* s, const GateGeom& gg) {
+  if (!g_tc_env || !g_tc8d_env || s->dtype != DSV_C128 || gg.k != 5) return false;
+  if (s->nbits - gg.k - gg.nctrl < 7) return false;
+  return device_has_tcgen05(s->device);
+}
+
+// Gate digits: the real embedding E (n = 2i + out re/im, kk = 2j + in re/im)
+// as X = rint(E 2^(51 - e_b)), |X| <= 2^51, and X + 0x0080808080808080 split
+// into balanced base-256 digits b0 (2^48, |b0| <= 8) .. b6; row n of the
+// 256 x 128 B table holds [b_(n/64) | b_(4 + n/64)] of output real n % 64.
+int apply_tc8d(dsv_state* s, const GateGeom& gg, const void* matrix, int prof_class, double bytes) {
+  constexpr int D = 32;
+  UnitView uv;
+  if (int rc = unit_view(s, gg, false, &uv)) return rc;
+  TcDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.g = uv.g;
+  for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
+  d.tshift = gg.tsorted[0];
+  for (int m = 1; m < gg.k; ++m)
+    if (gg.tsorted[m] != gg.tsorted[0] + m) d.tshift = -1;
+  std::vector<cplx<double>> m;
+  canon_matrix<double>(gg, matrix, m);
+  double bmax = 0.0;
+  for (const auto& z : m) bmax = std::max(bmax, std::max(std::fabs(z.x), std::fabs(z.y)));
+  if (!std::isfinite(bmax)) return fail(DSV_EINVAL, "matrix has non-finite entries");
+  int e_b = 0;
+  if (bmax > 0.0) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
+  d.e_b = e_b;
+  constexpr uint64_t kOff = 0x0080808080808080ull;
+  std::vector<unsigned char> host(256 * 128, 0);
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) {
+      const double re = m[size_t(i) * D + j].x, im = m[size_t(i) * D + j].y;
+      const double e[2][2] = {{re, -im}, {im, re}};
+      for (int oc = 0; oc < 2; ++oc)
+        for (int ic = 0; ic < 2; ++ic) {
+          const int n = 2 * i + oc, kk = 2 * j + ic;
+          const int64_t x = int64_t(std::nearbyint(std::ldexp(e[oc][ic], 51 - e_b)));
+          const uint64_t u = uint64_t(x) + kOff;
+          for (int pl = 0; pl < 7; ++pl) {
+            const unsigned char byte = static_cast<unsigned char>(((u >> (8 * (6 - pl))) & 255u) ^ 0x80u);
+            const int row = (pl < 4 ? pl : pl - 4) * 64 + n;
+            host[size_t(row) * 128 + (pl < 4 ? 0 : 64) + kk] = byte;
+          }
+        }
+    }
+  if (int rc = ensure_gdata(s, host.size())) return rc;
+  CK(h2d(s, s->gdata, host.data(), host.size()));
+  ProfTok t = prof_start(s);
+  CKL(launch_dense_tc8d(d, s->gdata, s->d, s->stream), 1);
+  prof_stop(s, t, prof_class, bytes);
+  return DSV_OK;
+}
+
 // Dense (+ optional pre-phase) window on the tensor cores; caller holds the device guard.
 int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::vector<PhaseTerm>& terms,
              int prof_class, double bytes) {
@@ -958,7 +1019,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env},     {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)
@@ -1241,6 +1302,7 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env));
   if ((k == 5 || k == 6 || tc4) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
+  if (tc8d_eligible(s, gg)) return apply_tc8d(s, gg, matrix, PC_DENSE_TC, bytes);
   bool ctl_bit0 = false;
   for (int c = 0; c < nctrl; ++c) ctl_bit0 = ctl_bit0 || cb[c] == 0;
   if (g_dblk8_env && s->dtype == DSV_C64 && k >= 2 && s->nbits >= 3 && gg.holes.back() < 3 && gg.holes[0] <= 1 &&

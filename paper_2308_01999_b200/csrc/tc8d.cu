@@ -1,0 +1,332 @@
+// tc8d.cu — complex128 5-qubit windows on the tensor cores through exact
+// 8-bit digits (tcgen05.mma kind::i8, int32 accumulation): the digit
+// arithmetic of tc8.cu / tc68.cu widened to fp64 precision.  Replaces
+// apply_dense_bits (reference statevec.py:44-60) for complex128 k = 5 fused
+// windows, which on the CUDA cores are FP64-FMA bound (2^(k-2) = 8 flop per
+// byte against a ~5 flop/B FP64 ridge: 0.31-0.34 of the copy peak).
+//
+// Arithmetic.  Each tile row (one amplitude group, 64 reals) is scaled by a
+// power of two so its largest |value| is < 2^51 and rounded to an integer I
+// with ONE fma against the magic M = 1.5 * 2^52.  The bits of M + I are
+// (0x4338 + s) 2^48 + (I mod 2^48) with s = I >> 48: bytes 0..5 are the
+// unsigned base-256 digits of I (planes 6..1, u8) and, after subtracting
+// 0x38 from byte 6, s is the signed top digit (plane 0, s8 in [-8, 8]) — no
+// integer work per value beyond that one subtraction.  The gate's real
+// embedding is split on the host into balanced signed digits b0 (|b0| <= 8)
+// .. b6 in [-128, 127].
+// Products a_i b_j with i + j = L accumulate exactly in int32 in level L
+// (|acc| < 2^24); levels 0..7 are kept (34 digit products), the dropped
+// levels >= 8 weigh ~2^-52 of the row-times-column scale; the rounding of
+// the inputs to 52-bit integers (2^-52 of the row maximum) is the same order:
+// a few times the native FP64 kernel's rounding error.
+// Readback: H = acc0 2^24 + acc1 2^16 + acc2 2^8 + acc3 and
+// Lo = acc4 2^24 + ... + acc7 are exact int64 (< 2^49), made doubles by the
+// same magic (bits(M) + H as a double, minus M) and combined with one fma:
+//   out = (H 2^32 + Lo) 2^(e_row + e_b - 62).
+//
+// Layout (one persistent CTA per SM, 256 threads, thread (row, half) owns
+// members 16 half .. 16 half + 15 of tile row `row`):
+//   * 2-stage cp.async ring of 64 KB tiles ([member][row] x 16 B);
+//   * A digits in shared memory, K-major 128-byte swizzled: block q holds
+//     planes 2q (bytes 0..63) and 2q + 1 (bytes 64..127) of all 128 rows;
+//   * gate digits: 256 rows x 128 B, row n: bytes 0..63 = plane n / 64
+//     (b0..b3) of output real n % 64, bytes 64..127 = plane 4 + n / 64 (b4..b6);
+//   * TMEM: the CTA's 512 columns = levels 0..7 x 64 output reals;
+//     a_i [b_j .. b_j'] lands on levels i + j .. i + j' (contiguous columns),
+//     so 23 MMAs (N = 64..256) cover the 34 products per 128-row tile.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "launch.h"
+#include "tcgen05.cuh"
+
+namespace dsv {
+
+using namespace tcx;
+
+struct Tc8dP {
+  Geom g;
+  uint64_t ntiles;
+  int e_b;
+  int tshift;
+  uint64_t offs[32];
+};
+
+struct Tc8dLayout {
+  static constexpr int D = 32;
+  static constexpr int B_OFF = 0;
+  static constexpr int B_BYTES = 256 * 128;        // 32 KB
+  static constexpr int A_OFF = B_OFF + B_BYTES;    // 4 blocks x 128 rows x 128 B
+  static constexpr int A_BYTES = 4 * 128 * 128;    // 64 KB
+  static constexpr int BAR = A_OFF + A_BYTES;      // MMA mbarrier + TMEM slot
+  static constexpr int MX = BAR + 128;             // row maxima [half][row] (high words of |double|)
+  static constexpr int RING = (MX + 2 * 128 * 4 + 1023) / 1024 * 1024;
+  static constexpr int STAGE = 128 * D * 16;       // 64 KB
+  static constexpr int NSTAGE = 2;
+  static constexpr int BYTES = RING + NSTAGE * STAGE;
+  static_assert(BYTES + 1024 <= 227 * 1024, "shared memory budget");
+};
+
+constexpr unsigned long long kMagicBitsD = 0x4338000000000000ull;  // bits of 1.5 * 2^52
+constexpr double kMagicD = 6755399441055744.0;                      // 1.5 * 2^52
+
+__device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+
+__device__ __forceinline__ void issue_mma8d(uint32_t sbase) {
+  using L = Tc8dLayout;
+  // A plane 0 signed (s in [-8, 7]), planes 1..6 unsigned bytes; B balanced signed digits
+  constexpr uint32_t S64 = idesc_i8<64, 1, 1>(), S192 = idesc_i8<192, 1, 1>(), S256 = idesc_i8<256, 1, 1>();
+  constexpr uint32_t U64 = idesc_i8<64, 0, 1>(), U128 = idesc_i8<128, 0, 1>(), U192 = idesc_i8<192, 0, 1>(),
+                     U256 = idesc_i8<256, 0, 1>();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    auto A = [&](int i) { return sw128_desc(sbase + L::A_OFF + (i >> 1) * 16384 + 64 * (i & 1) + 32 * s); };
+    // half 0: planes b0..b3 from row 64 j; half 1: planes b4..b6 from row 64 (j - 4)
+    auto B0 = [&](int j) { return sw128_desc(sbase + L::B_OFF + j * 64 * 128 + 32 * s); };
+    auto B1 = [&](int j) { return sw128_desc(sbase + L::B_OFF + (j - 4) * 64 * 128 + 64 + 32 * s); };
+    const uint32_t acc = s > 0 ? 1u : 0u;
+    auto col = [](int level) { return uint32_t(64 * level); };
+    if (s == 0) {
+      mma_ss_i8(col(0), A(0), B0(0), S64, 0u);    // level 0        (zeroes cols 0..63)
+    } else {
+      mma_ss_i8(col(0), A(0), B0(0), S256, 1u);   // levels 0..3
+    }
+    mma_ss_i8(col(1), A(1), B0(0), U256, acc);    // levels 1..4    (s = 0: zeroes cols 64..319)
+    mma_ss_i8(col(5), A(1), B1(4), U192, acc);    // levels 5..7    (s = 0: zeroes cols 320..511)
+    if (s == 0) mma_ss_i8(col(1), A(0), B0(1), S192, 1u);  // levels 1..3
+    mma_ss_i8(col(4), A(0), B1(4), S192, 1u);     // levels 4..6
+    mma_ss_i8(col(2), A(2), B0(0), U256, 1u);     // levels 2..5
+    mma_ss_i8(col(6), A(2), B1(4), U128, 1u);     // levels 6..7
+    mma_ss_i8(col(3), A(3), B0(0), U256, 1u);     // levels 3..6
+    mma_ss_i8(col(7), A(3), B1(4), U64, 1u);      // level 7
+    mma_ss_i8(col(4), A(4), B0(0), U256, 1u);     // levels 4..7
+    mma_ss_i8(col(5), A(5), B0(0), U192, 1u);     // levels 5..7
+    mma_ss_i8(col(6), A(6), B0(0), U128, 1u);     // levels 6..7
+  }
+}
+
+__global__ void __launch_bounds__(256, 1)
+k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, double2* __restrict__ sv) {
+  using L = Tc8dLayout;
+  constexpr int S = L::NSTAGE;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t raw_base = smem_u32(smem_raw);
+  const uint32_t sbase = (raw_base + 1023u) & ~1023u;
+  unsigned char* sm = smem_raw + (sbase - raw_base);
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int row = tid & 127;
+  const int half = tid >> 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);
+  const uint32_t bar = sbase + L::BAR;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // gate digits, host layout [256 rows][8 x 16 B] -> 128-byte swizzled rows
+  for (int i = tid; i < 256 * 8; i += 256) {
+    const int r = i / 8, c16 = i % 8;
+    *reinterpret_cast<uint4*>(sm + L::B_OFF + r * 128 + ((c16 ^ (r & 7)) << 4)) = bmat[i];
+  }
+
+  const uint64_t step = gridDim.x;
+  auto tile_of = [&](int i) { return uint64_t(blockIdx.x) + uint64_t(i) * step; };
+  const uint64_t e0 = expand(p.g, 0);
+  const uint64_t rowoff = expand(p.g, row) ^ e0;
+  auto issue = [&](int i) -> uint64_t {
+    const uint64_t tl = tile_of(i);
+    uint64_t tb = 0;
+    if (tl < p.ntiles) {
+      tb = expand(p.g, tl * 128);
+      const uint32_t st0 = sbase + L::RING + (i % S) * L::STAGE + row * 16;
+      const uint64_t b = tb | rowoff;
+      if (p.tshift >= 0) {
+        const double2* src = sv + b + (uint64_t(16 * half) << p.tshift);
+        const uint64_t stride = uint64_t(1) << p.tshift;
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) cp_async16(st0 + (16 * half + mm) * 2048, src + mm * stride);
+      } else {
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) {
+          const int j = 16 * half + mm;
+          cp_async16(st0 + j * 2048, sv + b + p.offs[j]);
+        }
+      }
+    }
+    cp_async_commit();
+    return tb;
+  };
+  uint32_t* mxs = reinterpret_cast<uint32_t*>(sm + L::MX);
+
+  uint64_t tq = issue(0);
+  cp_async_wait<0>();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (*tmem_slot != 0u) __trap();
+  const uint32_t tlane = uint32_t((warp & 3) * 32) << 16;
+
+  // out = (H 2^32 + Lo) 2^(e_row + e_b - 62); H, Lo exact int64 < 2^49
+  auto epilogue = [&](uint64_t b, int e_row) {
+    const double s_lo = pow2d(e_row + p.e_b - 62), s_hi = pow2d(e_row + p.e_b - 30);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const int c0 = 32 * half + 8 * q;  // output reals c0 .. c0 + 7 = members c0 / 2 .. + 3
+      uint32_t acc[8][8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) tmem_ld8(tlane + uint32_t(64 * l + c0), acc[l]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int l = 0; l < 8; ++l) reg_fence(acc[l]);
+      double o[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const long long H = (long long)int(acc[0][c]) * 16777216ll + (long long)int(acc[1][c]) * 65536ll +
+                            (long long)int(acc[2][c]) * 256ll + (long long)int(acc[3][c]) + (long long)kMagicBitsD;
+        const long long Lw = (long long)int(acc[4][c]) * 16777216ll + (long long)int(acc[5][c]) * 65536ll +
+                             (long long)int(acc[6][c]) * 256ll + (long long)int(acc[7][c]) + (long long)kMagicBitsD;
+        const double hd = __dadd_rn(__longlong_as_double(H), -kMagicD);
+        const double ld = __dadd_rn(__longlong_as_double(Lw), -kMagicD);
+        o[c] = __fma_rn(hd, s_hi, __dmul_rn(ld, s_lo));
+      }
+      const int m0 = c0 / 2;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double2* dst = p.tshift >= 0 ? sv + b + (uint64_t(m0 + i) << p.tshift) : sv + b + p.offs[m0 + i];
+        __stcs(dst, make_double2(o[2 * i], o[2 * i + 1]));
+      }
+    }
+  };
+
+  uint64_t prev_base = 0;
+  int prev_e = 0;
+  int it = 0;
+#pragma unroll 1
+  for (;; ++it) {
+    const uint64_t tile = tile_of(it);
+    if (tile >= p.ntiles) break;
+    const uint64_t tb_cur = tq;
+    tq = issue(it + 1);
+    const uint64_t base = tb_cur | rowoff;
+    const double2* raw = reinterpret_cast<const double2*>(sm + L::RING + (it % S) * L::STAGE) + row;
+    double v[32];
+#pragma unroll
+    for (int mm = 0; mm < 16; ++mm) {
+      const double2 x = raw[(16 * half + mm) * 128];
+      v[2 * mm] = x.x;
+      v[2 * mm + 1] = x.y;
+    }
+    uint32_t mx = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) mx = max(mx, uint32_t(__double2hiint(v[c])) & 0x7FFFFFFFu);
+    mxs[half * 128 + row] = mx;
+    __syncthreads();  // B1: both halves' maxima
+    mx = max(mx, mxs[(half ^ 1) * 128 + row]);
+    // |values| < 2^e_row; clamp keeps 2^(50 - e_row) and the output scales normal
+    const int e_row = min(max(int(mx >> 20) - 1022, -900), 900);
+    const double sc_in = pow2d(51 - e_row);
+    // digits straight from the bits of M + I (|I| <= 2^51, M = 1.5 * 2^52; bits(M + I) = bits(M) + I holds up to 2^53):
+    // bytes 0..5 are the unsigned base-256 digits of I mod 2^48 (planes 6..1,
+    // u8), byte 6 is 0x38 + s with s = I >> 48 in [-8, 7] (plane 0, s8 once
+    // 0x38 is subtracted from the high word, s in [-8, 8]).  Word g of plane i = the
+    // plane-i bytes of reals 4g .. 4g + 3.
+    uint32_t dg[7][8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double x = __fma_rn(v[4 * g + r], sc_in, kMagicD);
+        lo[r] = uint32_t(__double2loint(x));
+        hi[r] = uint32_t(__double2hiint(x)) - 0x00380000u;
+      }
+      const uint32_t t01 = __byte_perm(lo[0], lo[1], 0x5140), t23 = __byte_perm(lo[2], lo[3], 0x5140);
+      const uint32_t u01 = __byte_perm(lo[0], lo[1], 0x7362), u23 = __byte_perm(lo[2], lo[3], 0x7362);
+      const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
+      const uint32_t g01 = __byte_perm(hi[0], hi[1], 0x0062), g23 = __byte_perm(hi[2], hi[3], 0x0062);
+      dg[6][g] = __byte_perm(t01, t23, 0x5410);
+      dg[5][g] = __byte_perm(t01, t23, 0x7632);
+      dg[4][g] = __byte_perm(u01, u23, 0x5410);
+      dg[3][g] = __byte_perm(u01, u23, 0x7632);
+      dg[2][g] = __byte_perm(h01, h23, 0x5410);
+      dg[1][g] = __byte_perm(h01, h23, 0x7632);
+      dg[0][g] = __byte_perm(g01, g23, 0x5410);
+    }
+    if (it > 0) {  // MMA(i-1) done: A is free and its accumulators are ready
+      mbar_wait(bar, (it - 1) & 1);
+      fence_after();
+      epilogue(prev_base, prev_e);
+    }
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      unsigned char* rowp = sm + L::A_OFF + (i >> 1) * 16384 + row * 128;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c16 = 4 * (i & 1) + 2 * half + h;
+        *reinterpret_cast<uint4*>(rowp + ((c16 ^ (row & 7)) << 4)) =
+            make_uint4(dg[i][4 * h], dg[i][4 * h + 1], dg[i][4 * h + 2], dg[i][4 * h + 3]);
+      }
+    }
+    cp_async_wait<0>();  // tile i+1 landed (this thread's part)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A digits visible to the tensor core
+    fence_before();
+    __syncthreads();  // B2
+    if (tid == 0) {
+      fence_after();
+      issue_mma8d(sbase);
+      mma_commit(bar);
+    }
+    prev_base = base;
+    prev_e = e_row;
+  }
+  if (it > 0) {
+    mbar_wait(bar, (it - 1) & 1);
+    fence_after();
+    epilogue(prev_base, prev_e);
+  }
+  cp_async_wait<0>();
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512) : "memory");
+  }
+}
+
+int tc8d_smem_bytes() { return Tc8dLayout::BYTES + 1024; }
+
+cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cudaStream_t st) {
+  Tc8dP p;
+  std::memset(&p, 0, sizeof p);
+  p.g = d.g;
+  p.ntiles = d.g.nwork / 128;
+  p.e_b = d.e_b;
+  p.tshift = d.tshift;
+  for (int j = 0; j < 32; ++j) p.offs[j] = d.offs[j];
+  const int smem = tc8d_smem_bytes();
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc8d, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  uint64_t blocks = uint64_t(device_sm_count());
+  if (blocks > p.ntiles) blocks = p.ntiles;
+  if (blocks == 0) return cudaSuccess;
+  k_dense_tc8d<<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
+                                                    static_cast<double2*>(sv));
+  return cudaGetLastError();
+}
+
+}  // namespace dsv
