@@ -70,6 +70,7 @@ bool g_tc8d_env = [] {
   const char* e = std::getenv("DSV_TC8D");
   return !(e && e[0] == '0');
 }();
+bool g_tc8d512 = true;
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -596,6 +597,7 @@ int apply_tc8d(dsv_state* s, const GateGeom& gg, const void* matrix, int prof_cl
   int e_b = 0;
   if (bmax > 0.0) std::frexp(bmax, &e_b);  // bmax in [2^(e_b-1), 2^e_b)
   d.e_b = e_b;
+  d.ws = g_tc8d512 ? 1 : 0;  // 512-thread layout (4 parts per row); dsv_config_set("tc8d512", 0): 256
   constexpr uint64_t kOff = 0x0080808080808080ull;
   std::vector<unsigned char> host(256 * 128, 0);
   for (int i = 0; i < D; ++i)
@@ -1019,7 +1021,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)

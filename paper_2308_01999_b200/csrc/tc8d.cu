@@ -24,8 +24,13 @@
 // same magic (bits(M) + H as a double, minus M) and combined with one fma:
 //   out = (H 2^32 + Lo) 2^(e_row + e_b - 62).
 //
-// Layout (one persistent CTA per SM, 256 threads, thread (row, half) owns
-// members 16 half .. 16 half + 15 of tile row `row`):
+// Layout (one persistent CTA per SM, NT = 512 threads by default, 256 with
+// dsv_config_set("tc8d512", 0); P = NT / 128 parts per tile row):
+//   * loader / epilogue: thread (row = tid % 128, part = tid / 128) copies
+//     and stores members 32 part / P .. of tile row `row` (its TMEM lane);
+//   * converters: warp w takes rows 32 w / P .., the P lanes of a row share
+//     its maximum by shuffles (no block barrier) and publish the row exponent
+//     in shared memory for the epilogue;
 //   * 2-stage cp.async ring of 64 KB tiles ([member][row] x 16 B);
 //   * A digits in shared memory, K-major 128-byte swizzled: block q holds
 //     planes 2q (bytes 0..63) and 2q + 1 (bytes 64..127) of all 128 rows;
@@ -33,7 +38,19 @@
 //     (b0..b3) of output real n % 64, bytes 64..127 = plane 4 + n / 64 (b4..b6);
 //   * TMEM: the CTA's 512 columns = levels 0..7 x 64 output reals;
 //     a_i [b_j .. b_j'] lands on levels i + j .. i + j' (contiguous columns),
-//     so 23 MMAs (N = 64..256) cover the 34 products per 128-row tile.
+//     so 23 MMAs (N = 64..256) cover the 34 products per 128-row tile;
+//   * with index bit 0 a target, member pairs (2i, 2i + 1) leave as one
+//     32-byte store (STG.256): full sectors (n = 32, (0,5,11,19,28): 36 -> 33 ms).
+// Bound: the 23 MMAs read ~230 KB of shared memory per tile (A 4 KB + B
+// N x 32 B each), ~1800 cycles at 128 B/clk, and the single 512-column
+// accumulator serialises them with the epilogue's TMEM reads: 0.75-0.8 of the
+// copy peak on a dense random state.  Rejected on the same box (A/B at
+// n = 32): a warp-specialised split (8 converter + 4 epilogue warps, mbarrier
+// handshakes: 25 -> 29 ms), output-half TMEM split so half 0's MMAs overlap
+// half 1's epilogue (46 narrower MMAs: 25 -> 30 ms), a third ring stage
+// holding A in the consumed stage (25 -> 29 ms), member-fastest loads for
+// index-bit-0 windows (slower: the cp.async smem writes or per-unit row
+// offsets cost more than the sectors saved).
 #include <cmath>
 #include <cstring>
 
@@ -50,8 +67,11 @@ struct Tc8dP {
   uint64_t ntiles;
   int e_b;
   int tshift;
+  int mlo;  // targets occupy index bits 0 .. mlo - 1 (0: bit 0 free)
   uint64_t offs[32];
 };
+
+
 
 struct Tc8dLayout {
   static constexpr int D = 32;
@@ -60,8 +80,8 @@ struct Tc8dLayout {
   static constexpr int A_OFF = B_OFF + B_BYTES;    // 4 blocks x 128 rows x 128 B
   static constexpr int A_BYTES = 4 * 128 * 128;    // 64 KB
   static constexpr int BAR = A_OFF + A_BYTES;      // MMA mbarrier + TMEM slot
-  static constexpr int MX = BAR + 128;             // row maxima [half][row] (high words of |double|)
-  static constexpr int RING = (MX + 2 * 128 * 4 + 1023) / 1024 * 1024;
+  static constexpr int MX = BAR + 128;             // row exponents [3][128] int
+  static constexpr int RING = (MX + 3 * 128 * 4 + 1023) / 1024 * 1024;
   static constexpr int STAGE = 128 * D * 16;       // 64 KB
   static constexpr int NSTAGE = 2;
   static constexpr int BYTES = RING + NSTAGE * STAGE;
@@ -70,6 +90,11 @@ struct Tc8dLayout {
 
 constexpr unsigned long long kMagicBitsD = 0x4338000000000000ull;  // bits of 1.5 * 2^52
 constexpr double kMagicD = 6755399441055744.0;                      // 1.5 * 2^52
+
+// one 32-byte streaming store (STG.256)
+__device__ __forceinline__ void st_cs_v4d(void* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
 
 __device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
 
@@ -106,10 +131,17 @@ __device__ __forceinline__ void issue_mma8d(uint32_t sbase) {
   }
 }
 
-__global__ void __launch_bounds__(256, 1)
+// NT threads = P parts per tile row (P = 2: 256 threads, P = 4: 512 threads
+// with half the values per thread and twice the warps to hide latency)
+template <int NT>
+__global__ void __launch_bounds__(NT, 1)
 k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, double2* __restrict__ sv) {
   using L = Tc8dLayout;
   constexpr int S = L::NSTAGE;
+  constexpr int P = NT / 128;   // parts per row
+  constexpr int MP = 32 / P;    // members per part
+  constexpr int RP = 64 / P;    // reals per part
+  constexpr int RW = 32 / P;    // rows per warp in the input phase
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t raw_base = smem_u32(smem_raw);
   const uint32_t sbase = (raw_base + 1023u) & ~1023u;
@@ -117,7 +149,7 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int row = tid & 127;
-  const int half = tid >> 7;
+  const int part = tid >> 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L::BAR + 16);
   const uint32_t bar = sbase + L::BAR;
 
@@ -132,7 +164,7 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // gate digits, host layout [256 rows][8 x 16 B] -> 128-byte swizzled rows
-  for (int i = tid; i < 256 * 8; i += 256) {
+  for (int i = tid; i < 256 * 8; i += NT) {
     const int r = i / 8, c16 = i % 8;
     *reinterpret_cast<uint4*>(sm + L::B_OFF + r * 128 + ((c16 ^ (r & 7)) << 4)) = bmat[i];
   }
@@ -149,14 +181,14 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
       const uint32_t st0 = sbase + L::RING + (i % S) * L::STAGE + row * 16;
       const uint64_t b = tb | rowoff;
       if (p.tshift >= 0) {
-        const double2* src = sv + b + (uint64_t(16 * half) << p.tshift);
+        const double2* src = sv + b + (uint64_t(MP * part) << p.tshift);
         const uint64_t stride = uint64_t(1) << p.tshift;
 #pragma unroll
-        for (int mm = 0; mm < 16; ++mm) cp_async16(st0 + (16 * half + mm) * 2048, src + mm * stride);
+        for (int mm = 0; mm < MP; ++mm) cp_async16(st0 + (MP * part + mm) * 2048, src + mm * stride);
       } else {
 #pragma unroll
-        for (int mm = 0; mm < 16; ++mm) {
-          const int j = 16 * half + mm;
+        for (int mm = 0; mm < MP; ++mm) {
+          const int j = MP * part + mm;
           cp_async16(st0 + j * 2048, sv + b + p.offs[j]);
         }
       }
@@ -164,7 +196,6 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
     cp_async_commit();
     return tb;
   };
-  uint32_t* mxs = reinterpret_cast<uint32_t*>(sm + L::MX);
 
   uint64_t tq = issue(0);
   cp_async_wait<0>();
@@ -176,29 +207,36 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
   const uint32_t tlane = uint32_t((warp & 3) * 32) << 16;
 
   // out = (H 2^32 + Lo) 2^(e_row + e_b - 62); H, Lo exact int64 < 2^49
-  auto epilogue = [&](uint64_t b, int e_row) {
+  // chunk = 8 output reals starting at real c0 (members c0 / 2 .. + 3); level
+  // L of real c at TMEM column 64 L + c
+  auto load_chunk = [&](int c0, uint32_t (&acc)[8][8]) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) tmem_ld8(tlane + uint32_t(64 * l + c0), acc[l]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int l = 0; l < 8; ++l) reg_fence(acc[l]);
+  };
+  auto finish_chunk = [&](const uint32_t (&acc)[8][8], int c0, uint64_t b, int e_row) {
     const double s_lo = pow2d(e_row + p.e_b - 62), s_hi = pow2d(e_row + p.e_b - 30);
-#pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      const int c0 = 32 * half + 8 * q;  // output reals c0 .. c0 + 7 = members c0 / 2 .. + 3
-      uint32_t acc[8][8];
+    double o[8];
 #pragma unroll
-      for (int l = 0; l < 8; ++l) tmem_ld8(tlane + uint32_t(64 * l + c0), acc[l]);
-      tmem_wait_ld();
+    for (int c = 0; c < 8; ++c) {
+      const long long H = (long long)int(acc[0][c]) * 16777216ll + (long long)int(acc[1][c]) * 65536ll +
+                          (long long)int(acc[2][c]) * 256ll + (long long)int(acc[3][c]) + (long long)kMagicBitsD;
+      const long long Lw = (long long)int(acc[4][c]) * 16777216ll + (long long)int(acc[5][c]) * 65536ll +
+                           (long long)int(acc[6][c]) * 256ll + (long long)int(acc[7][c]) + (long long)kMagicBitsD;
+      const double hd = __dadd_rn(__longlong_as_double(H), -kMagicD);
+      const double ld = __dadd_rn(__longlong_as_double(Lw), -kMagicD);
+      o[c] = __fma_rn(hd, s_hi, __dmul_rn(ld, s_lo));
+    }
+    const int m0 = c0 / 2;
+    if (p.mlo >= 1) {  // index bit 0 a target: members 2i, 2i + 1 are one 32-byte sector
 #pragma unroll
-      for (int l = 0; l < 8; ++l) reg_fence(acc[l]);
-      double o[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const long long H = (long long)int(acc[0][c]) * 16777216ll + (long long)int(acc[1][c]) * 65536ll +
-                            (long long)int(acc[2][c]) * 256ll + (long long)int(acc[3][c]) + (long long)kMagicBitsD;
-        const long long Lw = (long long)int(acc[4][c]) * 16777216ll + (long long)int(acc[5][c]) * 65536ll +
-                             (long long)int(acc[6][c]) * 256ll + (long long)int(acc[7][c]) + (long long)kMagicBitsD;
-        const double hd = __dadd_rn(__longlong_as_double(H), -kMagicD);
-        const double ld = __dadd_rn(__longlong_as_double(Lw), -kMagicD);
-        o[c] = __fma_rn(hd, s_hi, __dmul_rn(ld, s_lo));
+      for (int i = 0; i < 4; i += 2) {
+        double2* dst = p.tshift >= 0 ? sv + b + (uint64_t(m0 + i) << p.tshift) : sv + b + p.offs[m0 + i];
+        st_cs_v4d(dst, o[2 * i], o[2 * i + 1], o[2 * i + 2], o[2 * i + 3]);
       }
-      const int m0 = c0 / 2;
+    } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         double2* dst = p.tshift >= 0 ? sv + b + (uint64_t(m0 + i) << p.tshift) : sv + b + p.offs[m0 + i];
@@ -206,9 +244,24 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
       }
     }
   };
+  // this thread's output reals RP part .. RP part + RP - 1
+  auto epilogue = [&](uint64_t b, int e_row) {
+#pragma unroll 1
+    for (int c0 = RP * part; c0 < RP * part + RP; c0 += 8) {
+      uint32_t acc[8][8];
+      load_chunk(c0, acc);
+      finish_chunk(acc, c0, b, e_row);
+    }
+  };
 
-  uint64_t prev_base = 0;
-  int prev_e = 0;
+  // input phase: warp w converts rows RW w .. RW w + RW - 1, lanes l, l + RW,
+  // ... share row RW w + l (parts 0 .. P - 1), so the row maximum is a
+  // shuffle; the epilogue keeps the TMEM lane mapping (row = tid & 127) and
+  // reads the row's exponent from shared memory (double-buffered per tile)
+  const int irow = RW * warp + (tid & (RW - 1));
+  const int ipart = (tid & 31) / RW;
+  int* ebuf = reinterpret_cast<int*>(sm + L::MX);  // [2][128] row exponents
+  uint64_t prev_tb = 0;
   int it = 0;
 #pragma unroll 1
   for (;; ++it) {
@@ -216,32 +269,32 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
     if (tile >= p.ntiles) break;
     const uint64_t tb_cur = tq;
     tq = issue(it + 1);
-    const uint64_t base = tb_cur | rowoff;
-    const double2* raw = reinterpret_cast<const double2*>(sm + L::RING + (it % S) * L::STAGE) + row;
-    double v[32];
+    const double2* raw = reinterpret_cast<const double2*>(sm + L::RING + (it % S) * L::STAGE) + irow;
+    double v[RP];
 #pragma unroll
-    for (int mm = 0; mm < 16; ++mm) {
-      const double2 x = raw[(16 * half + mm) * 128];
+    for (int mm = 0; mm < MP; ++mm) {
+      const double2 x = raw[(MP * ipart + mm) * 128];
       v[2 * mm] = x.x;
       v[2 * mm + 1] = x.y;
     }
     uint32_t mx = 0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) mx = max(mx, uint32_t(__double2hiint(v[c])) & 0x7FFFFFFFu);
-    mxs[half * 128 + row] = mx;
-    __syncthreads();  // B1: both halves' maxima
-    mx = max(mx, mxs[(half ^ 1) * 128 + row]);
-    // |values| < 2^e_row; clamp keeps 2^(50 - e_row) and the output scales normal
-    const int e_row = min(max(int(mx >> 20) - 1022, -900), 900);
-    const double sc_in = pow2d(51 - e_row);
-    // digits straight from the bits of M + I (|I| <= 2^51, M = 1.5 * 2^52; bits(M + I) = bits(M) + I holds up to 2^53):
-    // bytes 0..5 are the unsigned base-256 digits of I mod 2^48 (planes 6..1,
-    // u8), byte 6 is 0x38 + s with s = I >> 48 in [-8, 7] (plane 0, s8 once
-    // 0x38 is subtracted from the high word, s in [-8, 8]).  Word g of plane i = the
-    // plane-i bytes of reals 4g .. 4g + 3.
-    uint32_t dg[7][8];
+    for (int c = 0; c < RP; ++c) mx = max(mx, uint32_t(__double2hiint(v[c])) & 0x7FFFFFFFu);
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
+    for (int o = RW; o < 32; o *= 2) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    // |values| < 2^e_row; the clamp keeps 2^(51 - e_row) and the output scales normal
+    const int e_row = min(max(int(mx >> 20) - 1022, -900), 900);
+    if (ipart == 0) ebuf[(it & 1) * 128 + irow] = e_row;
+    const double sc_in = pow2d(51 - e_row);
+    // digits straight from the bits of M + I (|I| <= 2^51, M = 1.5 * 2^52;
+    // bits(M + I) = bits(M) + I holds up to 2^53): bytes 0..5 are the
+    // unsigned base-256 digits of I mod 2^48 (planes 6..1, u8), byte 6 is
+    // 0x38 + s with s = I >> 48 in [-8, 8] (plane 0, s8 once 0x38 is
+    // subtracted from the high word).  Word g of plane i = the plane-i bytes
+    // of reals 4g .. 4g + 3.
+    uint32_t dg[7][RP / 4];
+#pragma unroll
+    for (int g = 0; g < RP / 4; ++g) {
       uint32_t lo[4], hi[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -264,15 +317,15 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
     if (it > 0) {  // MMA(i-1) done: A is free and its accumulators are ready
       mbar_wait(bar, (it - 1) & 1);
       fence_after();
-      epilogue(prev_base, prev_e);
+      epilogue(prev_tb | rowoff, ebuf[((it - 1) & 1) * 128 + row]);
     }
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
-      unsigned char* rowp = sm + L::A_OFF + (i >> 1) * 16384 + row * 128;
+      unsigned char* rowp = sm + L::A_OFF + (i >> 1) * 16384 + irow * 128;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c16 = 4 * (i & 1) + 2 * half + h;
-        *reinterpret_cast<uint4*>(rowp + ((c16 ^ (row & 7)) << 4)) =
+      for (int h = 0; h < RP / 16; ++h) {
+        const int c16 = 4 * (i & 1) + (RP / 16) * ipart + h;
+        *reinterpret_cast<uint4*>(rowp + ((c16 ^ (irow & 7)) << 4)) =
             make_uint4(dg[i][4 * h], dg[i][4 * h + 1], dg[i][4 * h + 2], dg[i][4 * h + 3]);
       }
     }
@@ -285,13 +338,12 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
       issue_mma8d(sbase);
       mma_commit(bar);
     }
-    prev_base = base;
-    prev_e = e_row;
+    prev_tb = tb_cur;
   }
   if (it > 0) {
     mbar_wait(bar, (it - 1) & 1);
     fence_after();
-    epilogue(prev_base, prev_e);
+    epilogue(prev_tb | rowoff, ebuf[((it - 1) & 1) * 128 + row]);
   }
   cp_async_wait<0>();
   fence_before();
@@ -300,6 +352,20 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(512) : "memory");
   }
+}
+
+template <int NT>
+static cudaError_t tc8d_go(const Tc8dP& p, unsigned blocks, int smem, const void* d_bmat, void* sv, cudaStream_t st) {
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc8d<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  k_dense_tc8d<NT><<<blocks, NT, smem, st>>>(p, static_cast<const uint4*>(d_bmat), static_cast<double2*>(sv));
+  return cudaGetLastError();
 }
 
 int tc8d_smem_bytes() { return Tc8dLayout::BYTES + 1024; }
@@ -311,22 +377,16 @@ cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cud
   p.ntiles = d.g.nwork / 128;
   p.e_b = d.e_b;
   p.tshift = d.tshift;
+  while (p.mlo < 5 && d.offs[1 << p.mlo] == (uint64_t(1) << p.mlo)) ++p.mlo;  // targets 0 .. mlo - 1
   for (int j = 0; j < 32; ++j) p.offs[j] = d.offs[j];
   const int smem = tc8d_smem_bytes();
-  static bool attr_set[64] = {false};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_tc8d, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set[dev] = true;
-  }
   uint64_t blocks = uint64_t(device_sm_count());
   if (blocks > p.ntiles) blocks = p.ntiles;
   if (blocks == 0) return cudaSuccess;
-  k_dense_tc8d<<<unsigned(blocks), 256, smem, st>>>(p, static_cast<const uint4*>(d_bmat),
-                                                    static_cast<double2*>(sv));
-  return cudaGetLastError();
+  const unsigned nb = unsigned(blocks);
+  // 512 threads (4 parts per row): twice the warps of the 256-thread
+  // layout to hide latency, 0-4 % faster on the same box (tools/_tc8d_probe.py)
+  return d.ws ? tc8d_go<512>(p, nb, smem, d_bmat, sv, st) : tc8d_go<256>(p, nb, smem, d_bmat, sv, st);
 }
 
 }  // namespace dsv
