@@ -71,6 +71,7 @@ bool g_tc8d_env = [] {
   return !(e && e[0] == '0');
 }();
 bool g_tc8d512 = true;
+bool g_tc8_pair01 = true;  // tc8 windows with targets on index bits 0 and 1 (mode 3)
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -483,7 +484,12 @@ bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
   // rows are the lowest free bits: with bits 0 and 1 both holes, consecutive
   // rows sit >= 32 bytes apart and the per-row 8-byte copies waste sectors —
   // unless the targets are exactly bits 0..k-1 (contiguous tiles, mode 2)
-  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1 && tc_mode(gg) != 2) return false;
+  // (tc8, k <= 5: index bit 0 the lowest target moves member pairs as 16-byte
+  // units (mode 3), so bits 0 and 1 both targets are fine there: QV-33 k = 5
+  // windows on (0, 1, ..) 88 -> ~25 ms)
+  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1 && tc_mode(gg) != 2 &&
+      !(g_tc8_env && gg.k <= 5 && gg.tsorted[0] == 0 && gg.tsorted[1] == 1 && g_tc8_pair01))
+    return false;
   const int free_bits = s->nbits - gg.k - gg.nctrl;
   if (free_bits < 7) return false;
   return device_has_tcgen05(s->device);
@@ -1021,7 +1027,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512}, {"tc8_pair01", &g_tc8_pair01},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)
