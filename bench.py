@@ -345,6 +345,50 @@ def qft33_check(st, step, ops, samples: int = 1 << 20) -> dict:
     return out
 
 
+def c128_reference_fuser_leg(dev, n: int = 31) -> dict:
+    """What a drop-in caller of the reference gets for complex128: quantum
+    volume depth 30 through the reference's own fuser (FusionConfig(5, 6),
+    mostly 5-qubit windows), on the complex128 tensor-core kernel (tc8d.cu)
+    and, for comparison, on the FP64 CUDA cores (dsv_config_set("tc8d", 0))."""
+    from paper_2308_01999_b200 import _native as N
+    from paper_2308_01999_b200.circuits import gen_qv, to_gates
+    from paper_2308_01999_b200.fusion import FusionConfig, fuse
+    from paper_2308_01999_b200.statevec import StateVector
+
+    gates = to_gates(gen_qv(n, 30, seed=0))
+    ops = fuse(gates, FusionConfig(5, 6)).gates
+    sv = StateVector(n, dtype=np.complex128, device=dev)
+    nat = sv.native
+    out = {"n_qubits": n, "circuit_gates": len(gates), "ops": len(ops),
+           "ops_5_qubits": sum(1 for o in ops if len(o.targets) == 5)}
+    try:
+        for flag, key in ((1, "tensor_cores"), (0, "fp64_cuda_cores")):
+            N.config_set("tc8d", flag)
+            nat.set_basis(0)
+            sv.bit_map = list(range(n))
+            sv.apply(ops[0])
+            nat.set_basis(0)
+            sv.bit_map = list(range(n))
+            nat.sync()
+            nat.prof_reset()
+            nat.prof_enable(True)
+            nat.event_record(0)
+            for o in ops:
+                sv.apply(o)
+            nat.event_record(1)
+            ms = nat.event_elapsed(0, 1)
+            prof = nat.prof_read()
+            nat.prof_enable(False)
+            out[key] = {"gates_per_s": len(gates) / (ms / 1000.0), "ms_per_circuit": ms,
+                        "tensor_windows": prof.get("dense_tc", {}).get("count", 0),
+                        "norm_dev": abs(sv.norm_squared() - 1.0)}
+    finally:
+        N.config_set("tc8d", 1)
+        del sv, nat
+    out["speedup"] = out["tensor_cores"]["gates_per_s"] / out["fp64_cuda_cores"]["gates_per_s"]
+    return out
+
+
 def run_single(args) -> None:
     from paper_2308_01999_b200 import _native as N
     from paper_2308_01999_b200.statevec import StateVector
@@ -449,6 +493,10 @@ def run_single(args) -> None:
     legs["clocks"] = clocks2.stop()
     check = qft33_check(st, step, ops)
     del st, nat
+    try:
+        legs["qv31_c128_reference_fuser"] = c128_reference_fuser_leg(dev)
+    except Exception as e:  # a leg must not take the headline down
+        legs["qv31_c128_reference_fuser"] = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     # e2e through the public API: fuse on the host, allocate, run, read back probabilities
     from paper_2308_01999_b200.statevec import run_circuit_sv
