@@ -7,8 +7,10 @@
 Runs every tcgen05 kernel family once on a small state — tc8 (k = 4/5 int8
 digits: pair, row, row2 and contiguous-tile modes, plain and phased), tc68
 (k = 6), and with DSV_TC8=0 the bf16-limb tc.cu / tc6.cu — plus the
-low-bit, 64-byte-block and exchange kernels, and checks each result
-against the CPU oracle so a silent corruption under the tool also fails.
+low-bit, 64-byte-block and exchange kernels, the complex128 tensor-core
+kernel (tc8d, 256- and 512-thread layouts) and a CUDA-graph capture and
+replay, and checks each result against the CPU oracle so a silent
+corruption under the tool also fails.
 """
 
 import os
@@ -55,8 +57,35 @@ def main():
     sh.run(to_gates(gen_qft(n)))
     worst = max(worst, float(np.abs(sh.gather_logical() - O.run_circuit(to_gates(gen_qft(n)), n)).max()))
     sh.close()
-    print(f"sanitize run ok: max|d| {worst:.2e} (DSV_TC8={os.environ.get('DSV_TC8', '1')})")
-    assert worst < 1e-5
+    # complex128 k = 5 on the tensor cores (tc8d): both thread layouts, bit 0 free / a target
+    from paper_2308_01999_b200 import _native as N
+
+    st2 = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n))
+    st2 /= np.linalg.norm(st2)
+    worst128 = 0.0
+    for t512 in (1, 0):
+        N.config_set("tc8d512", t512)
+        for targets in ((3, 4, 5, 6, 7), (0, 2, 5, 9, 13), (1, 4, 6, 9, 12)):
+            m = G.random_unitary(32, rng)
+            sv = StateVector.from_amplitudes(st2)
+            sv.apply(G.DenseGate(m, targets))
+            want = st2.copy()
+            O.apply_dense(want, n, m, list(targets))
+            worst128 = max(worst128, float(np.abs(sv.amplitudes - want).max()))
+    N.config_set("tc8d512", 1)
+    # CUDA-graph capture and replay of a fold-fused QFT (baked per-gate tables)
+    sv = StateVector.from_amplitudes(st)
+    with sv.capture() as rec:
+        for op in fuse_fold(to_gates(gen_qft(n)), 5).ops:
+            sv.apply(op)
+    sv.amplitudes = st
+    sv.bit_map = list(rec.start_map)
+    rec.replay()
+    want = O.run_circuit(to_gates(gen_qft(n)), n, state=st.astype(np.complex128))
+    worst = max(worst, float(np.abs(sv.logical_amplitudes() - want).max()))
+    rec.close()
+    print(f"sanitize run ok: max|d| {worst:.2e} c64, {worst128:.2e} c128 (DSV_TC8={os.environ.get('DSV_TC8', '1')})")
+    assert worst < 1e-5 and worst128 < 1e-12
 
 
 if __name__ == "__main__":
