@@ -385,7 +385,7 @@ cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cud
   if (blocks == 0) return cudaSuccess;
   const unsigned nb = unsigned(blocks);
   // 512 threads (4 parts per row): twice the warps of the 256-thread
-  // layout to hide latency, 0-4 % faster on the same box (tools/_tc8d_probe.py)
+  // layout to hide latency, 0-4 % faster on the same box (tools/tc8d_probe.py)
   return d.ws ? tc8d_go<512>(p, nb, smem, d_bmat, sv, st) : tc8d_go<256>(p, nb, smem, d_bmat, sv, st);
 }
 
