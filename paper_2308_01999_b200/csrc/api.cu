@@ -573,6 +573,44 @@ bool build_tile_tmap(const dsv_state* s, const GateGeom& gg, TcDesc* d) {
   return r == CUDA_SUCCESS;
 }
 
+// Unit factors exp(i angle) per (index-byte chunk, byte value, slot) for a
+// phased window's terms (slots 0..k-1: member bits, k: every member), in the
+// state's precision: [nchunk][256][k + 1] complex.  chunk_shift[c] = 8 * byte.
+void unit_factor_tables(const std::vector<PhaseTerm>& terms, int k, bool c128, int* nchunk, int chunk_shift[8],
+                        std::vector<unsigned char>& raw) {
+  int chunk_of_byte[8];
+  for (int c = 0; c < 8; ++c) chunk_of_byte[c] = -1;
+  *nchunk = 0;
+  for (const PhaseTerm& t : terms) {
+    const int c = t.bit / 8;
+    if (chunk_of_byte[c] < 0) {
+      chunk_of_byte[c] = *nchunk;
+      chunk_shift[(*nchunk)++] = 8 * c;
+    }
+  }
+  const int S = k + 1;
+  const size_t nt = size_t(std::max(*nchunk, 1)) * 256 * S;
+  std::vector<double> tab(nt, 0.0);
+  for (const PhaseTerm& t : terms) {
+    const int ci = chunk_of_byte[t.bit / 8];
+    const int bb = t.bit % 8;
+    for (int v = 0; v < 256; ++v)
+      if ((v >> bb) & 1) tab[(size_t(ci) * 256 + v) * S + t.slot] += t.th;
+  }
+  const size_t es = c128 ? 16 : 8;
+  raw.assign(nt * es, 0);
+  for (size_t i = 0; i < nt; ++i) {
+    const double c = std::cos(tab[i]), sn = std::sin(tab[i]);
+    if (c128) {
+      reinterpret_cast<double*>(raw.data())[2 * i] = c;
+      reinterpret_cast<double*>(raw.data())[2 * i + 1] = sn;
+    } else {
+      reinterpret_cast<float*>(raw.data())[2 * i] = float(c);
+      reinterpret_cast<float*>(raw.data())[2 * i + 1] = float(sn);
+    }
+  }
+}
+
 // complex128 k = 5 dense window on the tensor cores (tc8d.cu)
 bool tc8d_eligible(const dsv_state* s, const GateGeom& gg) {
   if (!g_tc_env || !g_tc8d_env || s->dtype != DSV_C128 || gg.k != 5) return false;
@@ -584,7 +622,8 @@ bool tc8d_eligible(const dsv_state* s, const GateGeom& gg) {
 // as X = rint(E 2^(51 - e_b)), |X| <= 2^51, and X + 0x0080808080808080 split
 // into balanced base-256 digits b0 (2^48, |b0| <= 8) .. b6; row n of the
 // 256 x 128 B table holds [b_(n/64) | b_(4 + n/64)] of output real n % 64.
-int apply_tc8d(dsv_state* s, const GateGeom& gg, const void* matrix, int prof_class, double bytes) {
+int apply_tc8d(dsv_state* s, const GateGeom& gg, const void* matrix, const std::vector<PhaseTerm>& terms,
+               int prof_class, double bytes) {
   constexpr int D = 32;
   UnitView uv;
   if (int rc = unit_view(s, gg, false, &uv)) return rc;
@@ -622,10 +661,16 @@ int apply_tc8d(dsv_state* s, const GateGeom& gg, const void* matrix, int prof_cl
           }
         }
     }
+  // phased windows (fold fuser): unit-factor tables after the gate digits
+  std::vector<unsigned char> ftab;
+  if (!terms.empty()) {
+    unit_factor_tables(terms, gg.k, true, &d.nnib, d.nib_shift, ftab);
+    host.insert(host.end(), ftab.begin(), ftab.end());
+  }
   if (int rc = ensure_gdata(s, host.size())) return rc;
   CK(h2d(s, s->gdata, host.data(), host.size()));
   ProfTok t = prof_start(s);
-  CKL(launch_dense_tc8d(d, s->gdata, s->d, s->stream), 1);
+  CKL(launch_dense_tc8d(d, s->gdata, static_cast<const unsigned char*>(s->gdata) + 256 * 128, s->d, s->stream), 1);
   prof_stop(s, t, prof_class, bytes);
   return DSV_OK;
 }
@@ -1310,7 +1355,7 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env));
   if ((k == 5 || k == 6 || tc4) && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
-  if (tc8d_eligible(s, gg)) return apply_tc8d(s, gg, matrix, PC_DENSE_TC, bytes);
+  if (tc8d_eligible(s, gg)) return apply_tc8d(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   bool ctl_bit0 = false;
   for (int c = 0; c < nctrl; ++c) ctl_bit0 = ctl_bit0 || cb[c] == 0;
   if (g_dblk8_env && s->dtype == DSV_C64 && k >= 2 && s->nbits >= 3 && gg.holes.back() < 3 && gg.holes[0] <= 1 &&
@@ -1510,51 +1555,24 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
   DeviceGuard g(s->device);
   if (tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
+  if (tc8d_eligible(s, gg))
+    return apply_tc8d(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
   if (k > kDenseRegMaxK)  // the host layer then applies the phases as diagonal gates
     return fail(DSV_EUNSUPPORTED, "phased 6-qubit window needs the tensor-core path (complex64, >= 7 free bits)");
   if (low_eligible(s, gg))
     return apply_low(s, gg, matrix, terms, PC_DENSE_LOW, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
   UnitView uv;
   if (int rc = unit_view(s, gg, k <= 4, &uv)) return rc;
-  // active index bytes and the [nchunk][256][k+1] tables
-  int chunk_of_byte[8];
+  // active index bytes and the [nchunk][256][k+1] unit-factor tables
   PhasedDesc d;
   std::memset(&d, 0, sizeof d);
   d.g = uv.g;
   for (int j = 0; j < (1 << k); ++j) d.offs[j] = uv.offs[j];
-  for (int c = 0; c < 8; ++c) chunk_of_byte[c] = -1;
-  for (const Term& t : terms) {
-    const int c = t.bit / 8;
-    if (chunk_of_byte[c] < 0) {
-      chunk_of_byte[c] = d.nchunk;
-      d.chunk_shift[d.nchunk++] = 8 * c;
-    }
-  }
-  const int S = k + 1;
-  const size_t nt = size_t(std::max(d.nchunk, 1)) * 256 * S;
+  std::vector<unsigned char> raw;
+  unit_factor_tables(terms, k, s->dtype == DSV_C128, &d.nchunk, d.chunk_shift, raw);
   if (d.nchunk == 0) {  // no outside terms: still valid (plain dense), keep one zero chunk
     d.nchunk = 1;
     d.chunk_shift[0] = 0;
-  }
-  std::vector<double> tab(nt, 0.0);
-  for (const Term& t : terms) {
-    const int ci = chunk_of_byte[t.bit / 8];
-    const int bb = t.bit % 8;
-    for (int v = 0; v < 256; ++v)
-      if ((v >> bb) & 1) tab[(size_t(ci) * 256 + v) * S + t.slot] += t.th;
-  }
-  // unit factors exp(i angle) per (byte chunk, byte value, slot), computed in double
-  const size_t es = s->dtype == DSV_C128 ? 16 : 8;
-  std::vector<unsigned char> raw(nt * es);
-  for (size_t i = 0; i < nt; ++i) {
-    const double c = std::cos(tab[i]), sn = std::sin(tab[i]);
-    if (s->dtype == DSV_C128) {
-      reinterpret_cast<double*>(raw.data())[2 * i] = c;
-      reinterpret_cast<double*>(raw.data())[2 * i + 1] = sn;
-    } else {
-      reinterpret_cast<float*>(raw.data())[2 * i] = float(c);
-      reinterpret_cast<float*>(raw.data())[2 * i + 1] = float(sn);
-    }
   }
   if (int rc = ensure_gdata(s, raw.size())) return rc;
   CK(h2d(s, s->gdata, raw.data(), raw.size()));

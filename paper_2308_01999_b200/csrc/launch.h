@@ -72,7 +72,9 @@ int tc_smem_bytes(int k);
 cudaError_t launch_dense_tc68(const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv, cudaStream_t st);
 // complex128 k = 5 windows through 8-bit integer digits (tc8d.cu); d_bmat =
 // 256 rows x 128 B: row n = [plane n / 64 | plane 4 + n / 64] of output real n % 64
-cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cudaStream_t st);
+// d.nnib > 0: phased window, d_ftab = [d.nnib][256][6] double2 unit factors per
+// index byte at shifts d.nib_shift[] (phased.cu's tables)
+cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, const void* d_ftab, void* sv, cudaStream_t st);
 int tc8d_smem_bytes();
 // same windows through 8-bit integer digits (tc8.cu); d_bmat = [b2 | b1 | b0][2^(k+1) rows][128] int8
 cudaError_t launch_dense_tc8(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,

@@ -68,8 +68,15 @@ struct Tc8dP {
   int e_b;
   int tshift;
   int mlo;  // targets occupy index bits 0 .. mlo - 1 (0: bit 0 free)
+  int nchunk;               // PHASED: index bytes carrying phase terms
+  int chunk_shift[8];       // their amplitude-index shifts (8 c)
+  const double2* ftab;      // PHASED: [nchunk][256][6] unit factors exp(i angle) per (byte value, slot)
   uint64_t offs[32];
 };
+
+__device__ __forceinline__ double2 cmul_d(double2 a, double2 b) {
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
+}
 
 
 
@@ -133,7 +140,7 @@ __device__ __forceinline__ void issue_mma8d(uint32_t sbase) {
 
 // NT threads = P parts per tile row (P = 2: 256 threads, P = 4: 512 threads
 // with half the values per thread and twice the warps to hide latency)
-template <int NT>
+template <int NT, bool PHASED>
 __global__ void __launch_bounds__(NT, 1)
 k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, double2* __restrict__ sv) {
   using L = Tc8dLayout;
@@ -260,6 +267,7 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
   // reads the row's exponent from shared memory (double-buffered per tile)
   const int irow = RW * warp + (tid & (RW - 1));
   const int ipart = (tid & 31) / RW;
+  const uint64_t irowoff = expand(p.g, irow) ^ e0;  // PHASED: group index of row irow within its tile
   int* ebuf = reinterpret_cast<int*>(sm + L::MX);  // [2][128] row exponents
   uint64_t prev_tb = 0;
   int it = 0;
@@ -276,6 +284,43 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
       const double2 x = raw[(MP * ipart + mm) * 128];
       v[2 * mm] = x.x;
       v[2 * mm + 1] = x.y;
+    }
+    if constexpr (PHASED) {
+      // the fold fuser's pre-phase (phased.cu's model): member j of the row
+      // with group index x takes exp(i (gamma(x) + sum_m j_m alpha_m(x))); the
+      // slot factors F_s = exp(i alpha_s(x)) (F_5 = exp(i gamma(x))) are
+      // products of tabulated unit factors per index byte, applied factor by
+      // factor to this thread's MP members (no sin/cos on the device)
+      const uint64_t x = tb_cur | irowoff;
+      double2 F[6];
+#pragma unroll
+      for (int t = 0; t < 6; ++t) F[t] = make_double2(1.0, 0.0);
+#pragma unroll 1
+      for (int c = 0; c < p.nchunk; ++c) {
+        const double2* tr = p.ftab + (c * 256 + int((x >> p.chunk_shift[c]) & 255u)) * 6;
+#pragma unroll
+        for (int t = 0; t < 6; ++t) F[t] = cmul_d(F[t], __ldg(tr + t));
+      }
+      constexpr int LMP = MP == 16 ? 4 : (MP == 8 ? 3 : 2);
+      double2 base = F[5];
+#pragma unroll
+      for (int m = LMP; m < 5; ++m)
+        if (((MP * ipart) >> m) & 1) base = cmul_d(base, F[m]);
+      // members in Gray-code order: one factor (or its conjugate) per step
+      double2 f = base;
+#pragma unroll
+      for (int i = 0; i < MP; ++i) {
+        const int mm = i ^ (i >> 1);
+        if (i > 0) {
+          // the bit that changed (folds to a constant after unrolling)
+          const int m = (i & 1) ? 0 : ((i & 2) ? 1 : ((i & 4) ? 2 : 3));
+          const double2 q = m == 0 ? F[0] : (m == 1 ? F[1] : (m == 2 ? F[2] : F[3]));
+          f = cmul_d(f, ((mm >> m) & 1) ? q : make_double2(q.x, -q.y));
+        }
+        const double2 y = cmul_d(f, make_double2(v[2 * mm], v[2 * mm + 1]));
+        v[2 * mm] = y.x;
+        v[2 * mm + 1] = y.y;
+      }
     }
     uint32_t mx = 0;
 #pragma unroll
@@ -354,23 +399,23 @@ k_dense_tc8d(const __grid_constant__ Tc8dP p, const uint4* __restrict__ bmat, do
   }
 }
 
-template <int NT>
+template <int NT, bool PHASED>
 static cudaError_t tc8d_go(const Tc8dP& p, unsigned blocks, int smem, const void* d_bmat, void* sv, cudaStream_t st) {
   static bool attr_set[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_tc8d<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tc8d<NT, PHASED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set[dev] = true;
   }
-  k_dense_tc8d<NT><<<blocks, NT, smem, st>>>(p, static_cast<const uint4*>(d_bmat), static_cast<double2*>(sv));
+  k_dense_tc8d<NT, PHASED><<<blocks, NT, smem, st>>>(p, static_cast<const uint4*>(d_bmat), static_cast<double2*>(sv));
   return cudaGetLastError();
 }
 
 int tc8d_smem_bytes() { return Tc8dLayout::BYTES + 1024; }
 
-cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cudaStream_t st) {
+cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, const void* d_ftab, void* sv, cudaStream_t st) {
   Tc8dP p;
   std::memset(&p, 0, sizeof p);
   p.g = d.g;
@@ -379,6 +424,9 @@ cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cud
   p.tshift = d.tshift;
   while (p.mlo < 5 && d.offs[1 << p.mlo] == (uint64_t(1) << p.mlo)) ++p.mlo;  // targets 0 .. mlo - 1
   for (int j = 0; j < 32; ++j) p.offs[j] = d.offs[j];
+  p.nchunk = d.nnib;  // byte chunks (TcDesc reuses its nibble fields)
+  for (int c = 0; c < d.nnib && c < 8; ++c) p.chunk_shift[c] = d.nib_shift[c];
+  p.ftab = static_cast<const double2*>(d_ftab);
   const int smem = tc8d_smem_bytes();
   uint64_t blocks = uint64_t(device_sm_count());
   if (blocks > p.ntiles) blocks = p.ntiles;
@@ -386,7 +434,9 @@ cudaError_t launch_dense_tc8d(const TcDesc& d, const void* d_bmat, void* sv, cud
   const unsigned nb = unsigned(blocks);
   // 512 threads (4 parts per row): twice the warps of the 256-thread
   // layout to hide latency, 0-4 % faster on the same box (tools/tc8d_probe.py)
-  return d.ws ? tc8d_go<512>(p, nb, smem, d_bmat, sv, st) : tc8d_go<256>(p, nb, smem, d_bmat, sv, st);
+  if (p.nchunk > 0)
+    return d.ws ? tc8d_go<512, true>(p, nb, smem, d_bmat, sv, st) : tc8d_go<256, true>(p, nb, smem, d_bmat, sv, st);
+  return d.ws ? tc8d_go<512, false>(p, nb, smem, d_bmat, sv, st) : tc8d_go<256, false>(p, nb, smem, d_bmat, sv, st);
 }
 
 }  // namespace dsv

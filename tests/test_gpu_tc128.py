@@ -114,3 +114,37 @@ def test_tc8d_deep_circuit_matches_fp64():
     assert_state_close(outs[0], want, np.complex128)
     assert np.abs(outs[0] - outs[1]).max() <= 1e-13
     assert abs(np.vdot(outs[0], outs[0]).real - 1.0) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [14, 17])
+def test_tc8d_phased_fold_windows(n):
+    """The fold fuser's phased 5-qubit windows (pre-phase from unit-factor
+    tables per index byte) on tc8d: complex128 QFT from a random state vs the
+    oracle and vs the FP64 CUDA-core phased kernel."""
+    from paper_2308_01999_b200.circuits import gen_qft, to_gates
+    from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+    rng = np.random.default_rng(n)
+    st = random_state(n, rng, np.complex128)
+    gates = to_gates(gen_qft(n))
+    ops = fuse_fold(gates, 5).ops
+    outs = []
+    for flag in (1, 0):
+        N.config_set("tc8d", flag)
+        try:
+            sv = StateVector.from_amplitudes(st)
+            nat = sv.native
+            nat.prof_reset()
+            nat.prof_enable(True)
+            for op in ops:
+                sv.apply(op)
+            prof = nat.prof_read()
+            nat.prof_enable(False)
+            outs.append(sv.logical_amplitudes())
+            if flag:
+                assert prof.get("dense_tc", {}).get("count", 0) >= 2, prof
+        finally:
+            N.config_set("tc8d", 1)
+    want = O.run_circuit(gates, n, state=st)
+    assert_state_close(outs[0], want, np.complex128)
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-13
