@@ -482,7 +482,9 @@ def run_single(args) -> None:
     qv_gates = to_gates(gen_qv(N_QUBITS, 30, seed=0))
     qv_ops = fuse_auto(qv_gates, FOLD_K).ops  # cluster fuser: 130 windows (fold / reference: 152)
     rnd = random_gate_sequence(N_QUBITS, 200, np.random.default_rng(0), max_arity=2)
-    for name, circ, lops in (("qv33_c64_fused5", qv_gates, qv_ops), ("random33_c64", rnd, rnd)):
+    rnd_ops = fuse_auto(rnd, FOLD_K).ops  # the same 200 gates in <= 5-qubit windows
+    for name, circ, lops in (("qv33_c64_fused5", qv_gates, qv_ops), ("random33_c64", rnd, rnd),
+                             ("random33_c64_fused5", rnd, rnd_ops)):
         step(lops)
         nat.event_record(2)
         step(lops)
@@ -637,6 +639,15 @@ def _run_legs(legs: dict, P: int, devices, shift: int) -> None:
                "norm": s5.norm_squared(), "exchange": _exchange_gbs(pf)}
         s5.close()
         del s5
+        # the same 200 gates in <= 5-qubit windows (host fusion is part of the
+        # reference pipeline too: its CLI fuses before running)
+        rnd36_ops = fuse_auto(rnd36, 5).ops
+        s5f = ShardedStateVector(n5, devices, np.complex64)
+        ms36f = _sharded_time(s5f, rnd36_ops, 1, 1)
+        leg["fused5"] = {"gates_per_s": len(rnd36) / (ms36f / 1000.0), "ms_per_circuit": ms36f,
+                         "fused_ops": len(rnd36_ops), "transfer_stats": s5f.stats.as_dict()}
+        s5f.close()
+        del s5f
         if P == 8:
             rnd33 = random_gate_sequence(n5 - 3, 200, np.random.default_rng(0), max_arity=2)
             s1 = ShardedStateVector(n5 - 3, [devices[0]], np.complex64)
