@@ -611,6 +611,21 @@ void unit_factor_tables(const std::vector<PhaseTerm>& terms, int k, bool c128, i
   }
 }
 
+// every entry of the k-qubit matrix (state dtype) finite?
+bool matrix_finite(const dsv_state* s, const void* matrix, int k) {
+  const size_t n = size_t(2) << (2 * k);  // re + im
+  if (s->dtype == DSV_C128) {
+    const double* m = static_cast<const double*>(matrix);
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(m[i])) return false;
+  } else {
+    const float* m = static_cast<const float*>(matrix);
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(m[i])) return false;
+  }
+  return true;
+}
+
 // complex128 k = 5 dense window on the tensor cores (tc8d.cu)
 bool tc8d_eligible(const dsv_state* s, const GateGeom& gg) {
   if (!g_tc_env || !g_tc8d_env || s->dtype != DSV_C128 || gg.k != 5) return false;
@@ -1353,9 +1368,13 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   // cores: 2 TB/s) and with index bit 0 a target (16-byte member pairs on the
   // tensor path: (0,5,17,30) 28.0 -> 22.6 ms)
   const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env));
-  if ((k == 5 || k == 6 || tc4) && tc_eligible(s, gg))
+  // the digit kernels scale by the matrix's largest entry: a non-finite
+  // matrix (unitary=False callers) takes the CUDA cores, which propagate
+  // NaN / inf like the reference's NumPy product
+  const bool finite = matrix_finite(s, matrix, k);
+  if ((k == 5 || k == 6 || tc4) && finite && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, {}, PC_DENSE_TC, bytes);
-  if (tc8d_eligible(s, gg)) return apply_tc8d(s, gg, matrix, {}, PC_DENSE_TC, bytes);
+  if (finite && tc8d_eligible(s, gg)) return apply_tc8d(s, gg, matrix, {}, PC_DENSE_TC, bytes);
   bool ctl_bit0 = false;
   for (int c = 0; c < nctrl; ++c) ctl_bit0 = ctl_bit0 || cb[c] == 0;
   if (g_dblk8_env && s->dtype == DSV_C64 && k >= 2 && s->nbits >= 3 && gg.holes.back() < 3 && gg.holes[0] <= 1 &&
@@ -1553,9 +1572,10 @@ int dsv_apply_matrix_phased(dsv_state* s, const void* matrix, const int32_t* tar
     terms.push_back({k, b, out_theta[y]});
   }
   DeviceGuard g(s->device);
-  if (tc_eligible(s, gg))
+  const bool finite = matrix_finite(s, matrix, k);
+  if (finite && tc_eligible(s, gg))
     return apply_tc(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
-  if (tc8d_eligible(s, gg))
+  if (finite && tc8d_eligible(s, gg))
     return apply_tc8d(s, gg, matrix, terms, PC_DENSE_TC, 2.0 * double(amp_bytes(s->dtype)) * double(namps(s)));
   if (k > kDenseRegMaxK)  // the host layer then applies the phases as diagonal gates
     return fail(DSV_EUNSUPPORTED, "phased 6-qubit window needs the tensor-core path (complex64, >= 7 free bits)");

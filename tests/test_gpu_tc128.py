@@ -148,3 +148,25 @@ def test_tc8d_phased_fold_windows(n):
     want = O.run_circuit(gates, n, state=st)
     assert_state_close(outs[0], want, np.complex128)
     assert np.abs(outs[0] - outs[1]).max() <= 1e-13
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_nonfinite_matrix_propagates_like_numpy(dtype):
+    """A non-finite matrix (unitary=False) must not go through the digit
+    kernels (they scale by the largest entry): it takes the CUDA cores and
+    NaN / inf propagate as in the reference's NumPy product."""
+    n = 12
+    rng = np.random.default_rng(3)
+    st = random_state(n, rng, dtype)
+    m = G.random_unitary(32, rng)
+    m[3, 7] = np.nan
+    g = G.DenseGate(m, (2, 4, 6, 8, 10), unitary=False)
+    sv = StateVector.from_amplitudes(st)
+    sv.apply(g)
+    want = st.astype(np.complex128)
+    O.apply_gate(want, n, G.DenseGate(np.asarray(m, dtype=dtype).astype(np.complex128), g.targets, unitary=False))
+    got = sv.amplitudes
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    tol = 1e-5 if dtype == np.complex64 else 1e-12
+    assert np.abs(got[ok] - want[ok]).max() <= tol
