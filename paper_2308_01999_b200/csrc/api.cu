@@ -71,7 +71,14 @@ bool g_tc8d_env = [] {
   return !(e && e[0] == '0');
 }();
 bool g_tc8d512 = true;
-bool g_tc8_pair01 = true;  // tc8 windows with targets on index bits 0 and 1 (mode 3)
+bool g_tc8_pair01 = true;
+// tc8 two-group kernel, plain row-pair windows: pair-swapped 16-byte stores
+// (lane shuffles) instead of 8-byte row stores.  2 % faster on sparse data
+// (QFT's first window on |0>), 8-12 % slower on a dense random state (QV /
+// random circuits: (3,9,17,22,30) 27.0 -> 23.7 ms with 8-byte stores,
+// tools/_st8_probe.py): off by default.  (The warp-specialised kernel keeps
+// the pair-swapped stores: there they win on dense states, 31.5 -> 28.7 ms.)
+bool g_tc8_pairswap = false;  // tc8 windows with targets on index bits 0 and 1 (mode 3)
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -817,6 +824,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
     // a wash or up to 5 % slower (contiguous and phased windows, targets from
     // bit 3 up): DSV_TC8WS=0 disables it; dsv_config_set("tc8ws_all", 1)
     // forces it for A/B runs.
+    d.pairswap = g_tc8_pairswap ? 1 : 0;
     const bool ws_layout = (d.mode == 3 && g_tc8ws_row2) || (d.mode == 1 && gg.tsorted[0] <= 2);
     d.ws = (g_tc8ws_env && terms.empty() && (ws_layout || g_tc8ws_all)) ? 1 : 0;
     // TMA tile loads where they measured faster than the per-thread cp.async
@@ -1087,7 +1095,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512}, {"tc8_pair01", &g_tc8_pair01},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512}, {"tc8_pair01", &g_tc8_pair01}, {"tc8_pairswap", &g_tc8_pairswap},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)

@@ -64,6 +64,7 @@ struct TcDesc {
   CUtensorMap tmap;
   int tma_shift[5];          // coordinate of map dimension q = (tile >> shift[q]) & mask[q]
   uint32_t tma_mask[5];      // (mask 0: a row / member / padding dimension, coordinate 0)
+  int pairswap;              // tc8 plain row-pair windows: pair-swapped 16-byte stores (else 8-byte rows)
 };
 cudaError_t launch_dense_tc(int k, const TcDesc& d, const void* d_bmat, const void* d_tab, void* sv,
                             cudaStream_t st);

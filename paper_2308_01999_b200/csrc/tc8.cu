@@ -64,6 +64,7 @@ struct Tc8P {
   int nrb;                // row-phase bits (<= 3): per tile, 2^nrb vectors = tile vector x R_v
   int rb_bit[3];
   const float2* rvec;     // [2^nrb][D] launch-constant row phase factors
+  int pairswap;           // plain row-pair windows: lanes swap one member and store 16 bytes (A/B; default 8-byte rows)
 };
 
 template <int K>
@@ -340,7 +341,7 @@ k_dense_tc8(const __grid_constant__ Tc8P<K> p, const __grid_constant__ CUtensorM
         for (int i = 0; i < 8; ++i)
           __stcs(reinterpret_cast<float4*>(sv + b + p.offs[h * 16 + 2 * i]),
                  make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
-      } else if constexpr (PAIR && !PHASED) {
+      } else if (PAIR && !PHASED && p.pairswap) {
         // lanes 2t', 2t'+1 hold adjacent amplitudes: swap one member per pair
         // and store 16 bytes each (even lane: member 2q of both rows, odd: 2q+1)
         const bool odd = row & 1;
@@ -924,7 +925,7 @@ k_dense_tc8ws(const __grid_constant__ Tc8P<K> p, const uint4* __restrict__ bmat,
           for (int q = 0; q < 8; ++q)
             __stcs(reinterpret_cast<float4*>(sv + b + p.offs[h * 16 + 2 * q]),
                    make_float4(val(4 * q), val(4 * q + 1), val(4 * q + 2), val(4 * q + 3)));
-        } else if constexpr (PAIR && !PHASED) {
+        } else if constexpr (PAIR && !PHASED) {  // (pair-swapped stores win here: 31.5 -> 28.7 ms on (1,9,17,22,30), dense state)
           const bool odd = row & 1;
           const uint64_t be = b - (odd ? 1 : 0);
           float2* dst = sv + be + (p.tshift >= 0 ? (uint64_t(h * 16 + (odd ? 1 : 0)) << p.tshift) : 0);
@@ -981,6 +982,7 @@ static cudaError_t tc8_go(const TcDesc& d, const void* d_bmat, const void* d_tab
   std::memset(&p, 0, sizeof p);
   p.g = d.g;
   p.ntiles = d.g.nwork / 128;
+  p.pairswap = d.pairswap;
   p.nnib = d.nnib;
   p.e_b = d.e_b;
   // every power of two the kernel forms stays normal: 22 - e_row, e_row + e_b - 29, e_row + e_b - 7
