@@ -78,7 +78,8 @@ bool g_tc8_pair01 = true;
 // random circuits: (3,9,17,22,30) 27.0 -> 23.7 ms with 8-byte stores,
 // tools/_st8_probe.py): off by default.  (The warp-specialised kernel keeps
 // the pair-swapped stores: there they win on dense states, 31.5 -> 28.7 ms.)
-bool g_tc8_pairswap = false;  // tc8 windows with targets on index bits 0 and 1 (mode 3)
+bool g_tc8_pairswap = false;
+bool g_tc4_all = false;  // A/B: every complex64 k = 4 dense gate on the tensor cores  // tc8 windows with targets on index bits 0 and 1 (mode 3)
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
@@ -1095,7 +1096,7 @@ int dsv_config_set(const char* key, int value) {
   static const struct {
     const char* name;
     bool* flag;
-  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512}, {"tc8_pair01", &g_tc8_pair01}, {"tc8_pairswap", &g_tc8_pairswap},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
+  } kKeys[] = {{"tc", &g_tc_env},         {"tc8", &g_tc8_env},     {"tc8ws", &g_tc8ws_env}, {"tc8ws_all", &g_tc8ws_all}, {"tc8ws_row2", &g_tc8ws_row2},  {"tma", &g_tma_env}, {"rowvec", &g_rowvec_env}, {"tc8d", &g_tc8d_env}, {"tc8d512", &g_tc8d512}, {"tc8_pair01", &g_tc8_pair01}, {"tc8_pairswap", &g_tc8_pairswap}, {"tc4_all", &g_tc4_all},    {"low", &g_low_env}, {"lowt", &g_lowt_env},
                {"dblk8", &g_dblk8_env}, {"blk8", &g_blk8_env}, {"wt", &g_wt_env}};
   if (!key) return fail(DSV_EINVAL, "null key");
   for (const auto& k : kKeys)
@@ -1375,7 +1376,12 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   // of peak, the tensor path 0.77-0.88) except on the lowest four bits (CUDA
   // cores: 2 TB/s) and with index bit 0 a target (16-byte member pairs on the
   // tensor path: (0,5,17,30) 28.0 -> 22.6 ms)
-  const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env));
+  // contiguous targets from bit 7 up (rows = bits 0..6): tensor path 22.7 vs
+  // 26.2 ms on a dense state at n = 33 ((8,9,10,11), tools/_tc4_probe.py);
+  // scattered or low targets stay on the CUDA cores
+  bool contig_hi = g_tc8_env && gg.tsorted[0] >= 7 && gg.nctrl == 0;
+  for (int m = 1; m < k; ++m) contig_hi = contig_hi && gg.tsorted[m] == gg.tsorted[0] + m;
+  const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env) || contig_hi || g_tc4_all);
   // the digit kernels scale by the matrix's largest entry: a non-finite
   // matrix (unitary=False callers) takes the CUDA cores, which propagate
   // NaN / inf like the reference's NumPy product
