@@ -483,8 +483,9 @@ def run_single(args) -> None:
     qv_ops = fuse_auto(qv_gates, FOLD_K).ops  # cluster fuser: 130 windows (fold / reference: 152)
     rnd = random_gate_sequence(N_QUBITS, 200, np.random.default_rng(0), max_arity=2)
     rnd_ops = fuse_auto(rnd, FOLD_K).ops  # the same 200 gates in <= 5-qubit windows
-    for name, circ, lops in (("qv33_c64_fused5", qv_gates, qv_ops), ("random33_c64", rnd, rnd),
-                             ("random33_c64_fused5", rnd, rnd_ops)):
+    qv6_ops = fuse_auto(qv_gates, 6).ops  # 6-qubit windows (tc68.cu): 99 windows
+    for name, circ, lops in (("qv33_c64_fused5", qv_gates, qv_ops), ("qv33_c64_fused6", qv_gates, qv6_ops),
+                             ("random33_c64", rnd, rnd), ("random33_c64_fused5", rnd, rnd_ops)):
         step(lops)
         nat.event_record(2)
         step(lops)

@@ -488,15 +488,17 @@ int tc_mode(const GateGeom& gg) {
 bool tc_eligible(const dsv_state* s, const GateGeom& gg) {
   if (!g_tc_env || s->dtype != DSV_C64) return false;
   if (gg.k < 4 || gg.k > 6) return false;
-  if (gg.k == 6 && gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1) return false;  // no contiguous-tile mode at k = 6
+  // k = 6 with index bits 0 and 1 both holes: tc68's per-row 8-byte copies
+  // waste half of each sector, but the alternative is the generic CUDA-core
+  // kernel (QV-33 k = 6 windows: ~420 ms each there), so they stay here
   // rows are the lowest free bits: with bits 0 and 1 both holes, consecutive
   // rows sit >= 32 bytes apart and the per-row 8-byte copies waste sectors —
   // unless the targets are exactly bits 0..k-1 (contiguous tiles, mode 2)
   // (tc8, k <= 5: index bit 0 the lowest target moves member pairs as 16-byte
   // units (mode 3), so bits 0 and 1 both targets are fine there: QV-33 k = 5
   // windows on (0, 1, ..) 88 -> ~25 ms)
-  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1 && tc_mode(gg) != 2 &&
-      !(g_tc8_env && gg.k <= 5 && gg.tsorted[0] == 0 && gg.tsorted[1] == 1 && g_tc8_pair01))
+  if (gg.holes.size() >= 2 && gg.holes[0] == 0 && gg.holes[1] == 1 && tc_mode(gg) != 2 && gg.k <= 5 &&
+      !(g_tc8_env && gg.tsorted[0] == 0 && gg.tsorted[1] == 1 && g_tc8_pair01))
     return false;
   const int free_bits = s->nbits - gg.k - gg.nctrl;
   if (free_bits < 7) return false;

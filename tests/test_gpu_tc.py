@@ -309,7 +309,7 @@ def test_low_phased_complex128_vs_oracle(k):
 
 # ---- k = 6 windows (tc6.cu) -------------------------------------------------------------------
 
-@pytest.mark.parametrize("case", ["high", "mid", "spread", "bit0", "ctrl"])
+@pytest.mark.parametrize("case", ["high", "mid", "spread", "bit0", "ctrl", "bits01", "low6", "bit1"])
 def test_tc6_dense_vs_oracle(case):
     rng = np.random.default_rng(600 + len(case))
     n = 17
@@ -319,6 +319,9 @@ def test_tc6_dense_vs_oracle(case):
         "spread": ([2, 5, 8, 11, 13, 16], []),
         "bit0": ([0, 3, 6, 9, 12, 15], []),        # per-row 8-byte copies
         "ctrl": ([3, 6, 7, 9, 12, 14], [(16, 1)]),
+        "bits01": ([0, 1, 4, 7, 9, 12], []),       # both low bits targets (formerly the generic kernel)
+        "low6": ([0, 1, 2, 3, 4, 5], []),          # contiguous low window, per-row copies
+        "bit1": ([1, 3, 5, 8, 10, 12], []),        # member-parity lanes + pair-swapped stores
     }[case]
     targets = [int(t) for t in rng.permutation(targets)]
     st = random_state(n, rng, np.complex64)
