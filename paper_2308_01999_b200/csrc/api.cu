@@ -713,6 +713,7 @@ int apply_tc(dsv_state* s, const GateGeom& gg, const void* matrix, const std::ve
   d.mode = tc_mode(gg);
   // tc8 (k <= 5): index bit 0 the lowest target -> member pairs move as 16-byte units
   if (d.mode == 0 && k <= 5 && gg.tsorted[0] == 0 && g_tc8_env) d.mode = 3;  // kTcRow2 (tcgen05.cuh)
+  if ((d.mode == 0 || d.mode == 2) && k == 6 && gg.tsorted[0] == 0 && g_tc8_env) d.mode = 3;  // tc68.cu row2 (member pairs)
   for (int j = 0; j < D; ++j) d.offs[j] = uv.offs[j];
   d.tshift = gg.tsorted[0];
   for (int m = 1; m < k; ++m)

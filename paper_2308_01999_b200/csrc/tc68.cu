@@ -41,6 +41,7 @@ struct Tc68P {
   int coop;
   int tshift;
   int jpos;  // PAIR copies: thread-index bit that selects the member parity
+  int row2;  // !PAIR, index bit 0 the lowest target: member pairs (2m, 2m+1) move as 16-byte units
   int nib_shift[16];
   uint64_t offs[64];
   float4 ctab[kTcMaxNib * 16 * 2];
@@ -149,6 +150,13 @@ k_dense_tc68(const __grid_constant__ Tc68P p, const uint4* __restrict__ bmat, co
             cp_async16(st0 + j * 1024 + prow * 8, sv + b + p.offs[j]);
           }
         }
+      } else if (p.row2) {  // index bit 0 the lowest target: [member pair][row] x 16 B
+        const uint64_t b = tb | rowoff;
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) {
+          const int m = 16 * half + mm;
+          cp_async16(st0 + m * 2048 + row * 16, sv + b + p.offs[2 * m]);
+        }
       } else {  // index bit 0 a target or control: this thread's half row, 8 B per member
         const uint64_t b = tb | rowoff;
 #pragma unroll
@@ -226,7 +234,12 @@ k_dense_tc68(const __grid_constant__ Tc68P p, const uint4* __restrict__ bmat, co
         return combine(ch[c], cmid[c], __int2float_rn(__float_as_int(cl[c])), scale, cm);
       };
       const int jb = 32 * half + 16 * h;
-      if (PAIR && p.jpos == 0) {
+      if (!PAIR && p.row2) {  // member pairs (2m, 2m+1) are adjacent amplitudes: 16-byte stores
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          __stcs(reinterpret_cast<float4*>(sv + b + p.offs[jb + 2 * i]),
+                 make_float4(val(4 * i), val(4 * i + 1), val(4 * i + 2), val(4 * i + 3)));
+      } else if (PAIR && p.jpos == 0) {
         // lowest target at bit 1: rows (r, r+1) x members (m, m+1) are one
         // 32-byte sector held by lanes r, r+1 — swap one value per lane pair
         // and store 16 bytes each (even lane: member m of both rows, odd: m+1)
@@ -268,8 +281,18 @@ k_dense_tc68(const __grid_constant__ Tc68P p, const uint4* __restrict__ bmat, co
     const uint64_t base = tb_cur | rowoff;
     const float2* raw = reinterpret_cast<const float2*>(sm + L::RING + (it % S) * L::STAGE) + row;
     float2 v[32];
+    if (!PAIR && p.row2) {
+      const float4* raw2 = reinterpret_cast<const float4*>(sm + L::RING + (it % S) * L::STAGE) + row;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = raw[(32 * half + j) * 128];
+      for (int mm = 0; mm < 16; ++mm) {
+        const float4 x = raw2[(16 * half + mm) * 128];
+        v[2 * mm] = make_float2(x.x, x.y);
+        v[2 * mm + 1] = make_float2(x.z, x.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = raw[(32 * half + j) * 128];
+    }
     if constexpr (PHASED) {
       if (p.coop) {
 #pragma unroll
@@ -377,6 +400,7 @@ static cudaError_t tc68_go(const TcDesc& d, const void* d_bmat, const void* d_ta
   p.emax = std::min(100, 124 - d.e_b);
   p.coop = d.coop;
   p.tshift = d.tshift;
+  p.row2 = d.mode == kTcRow2 ? 1 : 0;
   p.jpos = 6;
   for (int lo = 0; lo < 7; ++lo)  // lowest target bit = lowest set bit of offs[1]
     if (d.offs[1] == (uint64_t(1) << lo)) p.jpos = lo >= 1 ? std::min(lo - 1, 6) : 6;
