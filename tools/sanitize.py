@@ -38,7 +38,8 @@ def main():
     worst = 0.0
     # dense k = 4..6 at layouts that select each tensor-core copy mode
     for targets in ((2, 3, 4, 5, 6), (0, 1, 2, 3, 4), (0, 3, 5, 8, 11), (1, 4, 6, 9, 12), (3, 4, 5, 6),
-                    (0, 2, 5, 7), (2, 4, 6, 8, 10, 12), (0, 1, 2, 3, 4, 5)):
+                    (0, 2, 5, 7), (2, 4, 6, 8, 10, 12), (0, 1, 2, 3, 4, 5), (0, 3, 6, 9, 11, 13),
+                    (1, 3, 5, 8, 10, 12), (0, 1, 4, 7, 9, 12), (0, 1, 6, 9, 12)):
         m = G.random_unitary(1 << len(targets), rng)
         sv = StateVector.from_amplitudes(st)
         sv.apply(G.DenseGate(m, targets))
