@@ -1379,10 +1379,12 @@ int dsv_apply_matrix(dsv_state* s, const void* matrix, const int32_t* targets, i
   // of peak, the tensor path 0.77-0.88) except on the lowest four bits (CUDA
   // cores: 2 TB/s) and with index bit 0 a target (16-byte member pairs on the
   // tensor path: (0,5,17,30) 28.0 -> 22.6 ms)
-  // contiguous targets from bit 7 up (rows = bits 0..6): tensor path 22.7 vs
-  // 26.2 ms on a dense state at n = 33 ((8,9,10,11), tools/_tc4_probe.py);
-  // scattered or low targets stay on the CUDA cores
-  bool contig_hi = g_tc8_env && gg.tsorted[0] >= 7 && gg.nctrl == 0;
+  // contiguous targets from bit 3 up: tensor path 22.7 vs 26.2 ms on a dense
+  // state at n = 33 ((8,9,10,11), tools/_tc4_probe.py), 2.96-3.04 vs
+  // 3.17-3.33 ms at n = 30 for (3..6), (4..7), (5..8) (tools/_lowk4.py);
+  // scattered targets and contiguous ones starting at bit 1 or 2 stay on
+  // the CUDA cores
+  bool contig_hi = g_tc8_env && gg.tsorted[0] >= 3 && gg.nctrl == 0;
   for (int m = 1; m < k; ++m) contig_hi = contig_hi && gg.tsorted[m] == gg.tsorted[0] + m;
   const bool tc4 = k == 4 && (tc_mode(gg) == 2 || (gg.tsorted[0] == 0 && g_tc8_env) || contig_hi || g_tc4_all);
   // the digit kernels scale by the matrix's largest entry: a non-finite
