@@ -444,3 +444,24 @@ def test_tc8_kernel_variants_all_layouts(targets):
                 N.config_set("tma", 1)
         for o in outs:
             assert _rel_err(o, want) <= 2 * REL
+
+
+# ---- routing added in round 2: layouts that formerly took the CUDA-core or generic kernels ----
+
+@pytest.mark.parametrize("targets", [
+    (3, 4, 5, 6), (8, 9, 10, 11),                 # k = 4, contiguous from bit 3 up -> tensor cores
+    (0, 1, 4, 7), (0, 1, 6, 9, 12), (0, 1, 2, 7, 11),   # targets on bits 0 and 1 (member-pair mode)
+    (0, 1, 4, 7, 9, 12), (0, 2, 5, 8, 10, 13),   # k = 6 with bit 0 a target (tc68 row2)
+])
+def test_round2_tensor_routing_vs_oracle(targets):
+    n = 15
+    rng = np.random.default_rng(sum(targets) + 31 * len(targets))
+    st = random_state(n, rng, np.complex64)
+    m = G.random_unitary(1 << len(targets), rng)
+    want = st.astype(np.complex128)
+    O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), list(targets), [])
+    sv = StateVector.from_amplitudes(st)
+    nat = _tc_launches(sv)
+    sv.apply_matrix(G.DenseGate(m, tuple(targets)))
+    assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1, nat.prof_read()
+    assert _rel_err(sv.amplitudes, want) <= REL, _rel_err(sv.amplitudes, want)
