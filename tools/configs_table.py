@@ -4,7 +4,8 @@ profile) beside the UNMODIFIED reference (baseline/_ref) on the host cores.
 
     python tools/configs_table.py > profiles/configs_table_r2.json
 
-GPU rows: config 1 (QFT-20 c128, unfused 220 gates and FusionConfig(5, 6)),
+GPU rows: config 1 (QFT-20 c128, unfused 220 gates and FusionConfig(5, 6),
+each also replayed as one CUDA graph),
 config 2 (random-30 c64, 200 gates unfused), config 3 is bench.py's line,
 configs 4 / 5 on ONE B200 as their per-GPU share (QV-33 c128 fold k = 4 =
 one segment of QV-34 on 2 GPUs; random-33 c64 = one segment of random-36 on
@@ -168,7 +169,11 @@ def main():
     g4 = to_gates(gen_qv(33, 30, seed=0))
     rows["4_qv33_c128_per_gpu"] = {"gpu_cluster_k4": gpu_run(33, fuse_auto(g4, 4).ops, np.complex128, len(g4), reps=1),
                                    "windows_cluster_k4": fuse_auto(g4, 4).data_passes,
-                                   "windows_fold_k4": fuse_fold(g4, 4).data_passes}
+                                   "windows_fold_k4": fuse_fold(g4, 4).data_passes,
+                                   # what a drop-in caller gets: the reference fuser's windows (mostly
+                                   # 5 qubits, on the complex128 tensor-core kernel tc8d.cu)
+                                   "gpu_reference_fuser_5_6": gpu_run(33, fuse(g4, FusionConfig(5, 6)).gates,
+                                                                      np.complex128, len(g4), reps=1)}
     rows["4_qv33_c128_per_gpu"]["cpu_reference"] = cpu_ref(
         26, ref_gates("qv", 26)[:CPU_GATES], np.complex128, full_n=34, full_count=510)
     # ---- config 5 per GPU: random-33 complex64 (one of the 8 segments of random-36)
