@@ -309,7 +309,7 @@ def test_low_phased_complex128_vs_oracle(k):
 
 # ---- k = 6 windows (tc6.cu) -------------------------------------------------------------------
 
-@pytest.mark.parametrize("case", ["high", "mid", "spread", "bit0", "ctrl", "bits01", "low6", "bit1"])
+@pytest.mark.parametrize("case", ["high", "mid", "spread", "bit0", "ctrl", "bits01", "low6", "bit1", "bit0ctrl"])
 def test_tc6_dense_vs_oracle(case):
     rng = np.random.default_rng(600 + len(case))
     n = 17
@@ -322,6 +322,7 @@ def test_tc6_dense_vs_oracle(case):
         "bits01": ([0, 1, 4, 7, 9, 12], []),       # both low bits targets (formerly the generic kernel)
         "low6": ([0, 1, 2, 3, 4, 5], []),          # contiguous low window, per-row copies
         "bit1": ([1, 3, 5, 8, 10, 12], []),        # member-parity lanes + pair-swapped stores
+        "bit0ctrl": ([0, 3, 6, 9, 12, 14], [(16, 1)]),  # row2 with a control
     }[case]
     targets = [int(t) for t in rng.permutation(targets)]
     st = random_state(n, rng, np.complex64)
@@ -453,15 +454,18 @@ def test_tc8_kernel_variants_all_layouts(targets):
     (0, 1, 4, 7), (0, 1, 6, 9, 12), (0, 1, 2, 7, 11),   # targets on bits 0 and 1 (member-pair mode)
     (0, 1, 4, 7, 9, 12), (0, 2, 5, 8, 10, 13),   # k = 6 with bit 0 a target (tc68 row2)
 ])
-def test_round2_tensor_routing_vs_oracle(targets):
+@pytest.mark.parametrize("ctrls", [(), ((14, 1),)])
+def test_round2_tensor_routing_vs_oracle(targets, ctrls):
     n = 15
+    if ctrls and len(targets) == 4 and targets[0] >= 3:
+        pytest.skip("controlled k = 4 gates stay on the CUDA cores")
     rng = np.random.default_rng(sum(targets) + 31 * len(targets))
     st = random_state(n, rng, np.complex64)
     m = G.random_unitary(1 << len(targets), rng)
     want = st.astype(np.complex128)
-    O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), list(targets), [])
+    O.apply_dense(want, n, m.astype(np.complex64).astype(np.complex128), list(targets), list(ctrls))
     sv = StateVector.from_amplitudes(st)
     nat = _tc_launches(sv)
-    sv.apply_matrix(G.DenseGate(m, tuple(targets)))
+    sv.apply_matrix(G.DenseGate(m, tuple(targets), tuple(ctrls)))
     assert nat.prof_read().get("dense_tc", {}).get("count", 0) == 1, nat.prof_read()
     assert _rel_err(sv.amplitudes, want) <= REL, _rel_err(sv.amplitudes, want)
