@@ -70,8 +70,8 @@ bool g_tc8d_env = [] {
   const char* e = std::getenv("DSV_TC8D");
   return !(e && e[0] == '0');
 }();
-bool g_tc8d512 = true;
-bool g_tc8_pair01 = true;
+bool g_tc8d512 = true;      // tc8d.cu: 512-thread layout (4 parts per row), else 256
+bool g_tc8_pair01 = true;   // tc8 windows with targets on index bits 0 and 1 (member-pair mode 3)
 // tc8 two-group kernel, plain row-pair windows: pair-swapped 16-byte stores
 // (lane shuffles) instead of 8-byte row stores.  2 % faster on sparse data
 // (QFT's first window on |0>), 8-12 % slower on a dense random state (QV /
@@ -79,7 +79,7 @@ bool g_tc8_pair01 = true;
 // tools/_st8_probe.py): off by default.  (The warp-specialised kernel keeps
 // the pair-swapped stores: there they win on dense states, 31.5 -> 28.7 ms.)
 bool g_tc8_pairswap = false;
-bool g_tc4_all = false;  // A/B: every complex64 k = 4 dense gate on the tensor cores  // tc8 windows with targets on index bits 0 and 1 (mode 3)
+bool g_tc4_all = false;  // A/B: every complex64 k = 4 dense gate on the tensor cores
 
 // Launch-constant row phase vectors for windows whose row-varying phases sit
 // on <= 3 tile-row bits (tc8.cu); DSV_ROWVEC=0 keeps the per-row sincos tree.
