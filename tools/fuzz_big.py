@@ -1,0 +1,78 @@
+#!/usr/bin/env python
+"""Large seeded fuzz of the B200 engine against the CPU oracle (a longer run
+of tests/test_gpu_fuzz.py's single-gate cases): random sizes 1..20, both
+dtypes, dense / diagonal / generalised-permutation gates of arity 1..7 with
+up to 2 controls, random states.  Permutations and diagonals must be
+bit-exact, dense gates within the north_star bars (conftest).
+
+    python tools/fuzz_big.py 3000 > profiles/fuzz_r2_big.txt
+"""
+import sys
+import time
+from collections import Counter
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+
+from conftest import assert_state_close, random_state  # noqa: E402
+from oracle import sv_oracle as O  # noqa: E402
+from paper_2308_01999_b200 import _native as N  # noqa: E402
+from paper_2308_01999_b200 import gates as G  # noqa: E402
+from paper_2308_01999_b200.statevec import StateVector  # noqa: E402
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    rng = np.random.default_rng(20261017)
+    kinds, classes, fails = Counter(), Counter(), []
+    t0 = time.time()
+    for c in range(cases):
+        n = int(rng.integers(1, 21))
+        dtype = (np.complex64, np.complex128)[int(rng.integers(0, 2))]
+        k = int(rng.integers(1, min(7, n) + 1))
+        qs = [int(q) for q in rng.permutation(n)]
+        targets = tuple(qs[:k])
+        nc = int(rng.integers(0, min(2, n - k) + 1))
+        ctrls = tuple((qs[k + i], int(rng.integers(0, 2))) for i in range(nc))
+        kind = int(rng.integers(0, 3))
+        if kind == 0:
+            g = G.DenseGate(G.random_unitary(1 << k, rng), targets, ctrls)
+        else:
+            perm = np.arange(1 << k) if kind == 1 else rng.permutation(1 << k)
+            g = G.PermutationGate(perm, np.exp(1j * rng.uniform(0, 6.3, 1 << k)), targets, ctrls)
+        st = random_state(n, rng, dtype)
+        sv = StateVector.from_amplitudes(st)
+        nat = sv.native
+        nat.prof_reset()
+        nat.prof_enable(True)
+        sv.apply(g)
+        for cl in nat.prof_read():
+            classes[cl] += 1
+        nat.prof_enable(False)
+        kinds[("dense", "diag", "perm")[kind], np.dtype(dtype).name, k] += 1
+        try:
+            if kind == 0:
+                ref = st.astype(np.complex128)
+                O.apply_gate(ref, n, G.DenseGate(np.asarray(g.matrix, dtype=dtype).astype(np.complex128), g.targets,
+                                                 g.controls, unitary=False))
+                assert_state_close(sv.amplitudes, ref, dtype)
+            else:
+                want = st.copy()
+                O.apply_gate(want, n, g)
+                np.testing.assert_array_equal(sv.amplitudes, want)
+        except AssertionError as e:
+            fails.append((c, n, np.dtype(dtype).name, kind, targets, ctrls, str(e)[:200]))
+    print(f"fuzz: {cases} cases in {time.time() - t0:.0f} s, {len(fails)} failures")
+    print("kernel classes hit:", dict(sorted(classes.items())))
+    print("gate kinds:", len(kinds), "distinct (kind, dtype, arity) combinations")
+    for f in fails[:20]:
+        print("FAIL", f)
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
