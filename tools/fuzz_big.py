@@ -6,6 +6,7 @@ up to 2 controls, random states.  Permutations and diagonals must be
 bit-exact, dense gates within the north_star bars (conftest).
 
     python tools/fuzz_big.py 3000 > profiles/fuzz_r2_big.txt
+    python tools/fuzz_big.py 400 circuits   # fused circuits (fold / cluster, k = 3..6)
 """
 import sys
 import time
@@ -74,5 +75,50 @@ def main():
     sys.exit(1 if fails else 0)
 
 
+def circuits():
+    """Random circuits and QFTs through the fold and cluster fusers (phased
+    windows on every tensor-core kernel) against the unfused oracle."""
+    from paper_2308_01999_b200.circuits import gen_qft, gen_qv, random_gate_sequence, to_gates
+    from paper_2308_01999_b200.fusion_cluster import fuse_cluster
+    from paper_2308_01999_b200.fusion_fold import fuse_fold
+
+    cases = int(sys.argv[1])
+    rng = np.random.default_rng(20261018)
+    classes, fails = Counter(), []
+    t0 = time.time()
+    for c in range(cases):
+        n = int(rng.integers(8, 19))
+        dtype = (np.complex64, np.complex128)[c % 2]
+        which = int(rng.integers(0, 3))
+        gates = (random_gate_sequence(n, 40, rng, max_arity=3) if which == 0 else
+                 to_gates(gen_qft(n)) if which == 1 else to_gates(gen_qv(n, 4, seed=int(rng.integers(0, 1 << 30)))))
+        k = int(rng.integers(3, 7))
+        fuser = (fuse_fold, fuse_cluster)[int(rng.integers(0, 2))]
+        ops = fuser(gates, k).ops
+        st = random_state(n, rng, dtype)
+        sv = StateVector.from_amplitudes(st)
+        nat = sv.native
+        nat.prof_reset()
+        nat.prof_enable(True)
+        for op in ops:
+            sv.apply(op)
+        for cl in nat.prof_read():
+            classes[cl] += 1
+        nat.prof_enable(False)
+        want = O.run_circuit(gates, n, state=st.astype(np.complex128))
+        try:
+            assert_state_close(sv.logical_amplitudes(), want, dtype)
+        except AssertionError as e:
+            fails.append((c, n, np.dtype(dtype).name, which, k, fuser.__name__, str(e)[:200]))
+    print(f"circuit fuzz: {cases} circuits in {time.time() - t0:.0f} s, {len(fails)} failures")
+    print("kernel classes hit:", dict(sorted(classes.items())))
+    for f in fails[:20]:
+        print("FAIL", f)
+    sys.exit(1 if fails else 0)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[2] == "circuits":
+        circuits()
+    else:
+        main()
