@@ -8,7 +8,8 @@ Runs every tcgen05 kernel family once on a small state — tc8 (k = 4/5 int8
 digits: pair, row, row2 and contiguous-tile modes, plain and phased), tc68
 (k = 6), and with DSV_TC8=0 the bf16-limb tc.cu / tc6.cu — plus the
 low-bit, 64-byte-block and exchange kernels, the complex128 tensor-core
-kernel (tc8d, 256- and 512-thread layouts) and a CUDA-graph capture and
+kernel (tc8d, 256- and 512-thread layouts), the batched k = 6 / 7 kernel
+and a CUDA-graph capture and
 replay, and checks each result against the CPU oracle so a silent
 corruption under the tool also fails.
 """
@@ -39,7 +40,7 @@ def main():
     # dense k = 4..6 at layouts that select each tensor-core copy mode
     for targets in ((2, 3, 4, 5, 6), (0, 1, 2, 3, 4), (0, 3, 5, 8, 11), (1, 4, 6, 9, 12), (3, 4, 5, 6),
                     (0, 2, 5, 7), (2, 4, 6, 8, 10, 12), (0, 1, 2, 3, 4, 5), (0, 3, 6, 9, 11, 13),
-                    (1, 3, 5, 8, 10, 12), (0, 1, 4, 7, 9, 12), (0, 1, 6, 9, 12)):
+                    (1, 3, 5, 8, 10, 12), (0, 1, 4, 7, 9, 12), (0, 1, 6, 9, 12), (1, 2, 4, 6, 8, 10, 13)):
         m = G.random_unitary(1 << len(targets), rng)
         sv = StateVector.from_amplitudes(st)
         sv.apply(G.DenseGate(m, targets))
@@ -66,8 +67,8 @@ def main():
     worst128 = 0.0
     for t512 in (1, 0):
         N.config_set("tc8d512", t512)
-        for targets in ((3, 4, 5, 6, 7), (0, 2, 5, 9, 13), (1, 4, 6, 9, 12)):
-            m = G.random_unitary(32, rng)
+        for targets in ((3, 4, 5, 6, 7), (0, 2, 5, 9, 13), (1, 4, 6, 9, 12), (0, 2, 4, 6, 8, 10)):
+            m = G.random_unitary(1 << len(targets), rng)
             sv = StateVector.from_amplitudes(st2)
             sv.apply(G.DenseGate(m, targets))
             want = st2.copy()
