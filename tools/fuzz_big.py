@@ -7,6 +7,7 @@ bit-exact, dense gates within the north_star bars (conftest).
 
     python tools/fuzz_big.py 3000 > profiles/fuzz_r2_big.txt
     python tools/fuzz_big.py 400 circuits   # fused circuits (fold / cluster, k = 3..6)
+    python tools/fuzz_big.py 300 shards     # sharded engine, P = 2..8 segments
 """
 import sys
 import time
@@ -117,8 +118,41 @@ def circuits():
     sys.exit(1 if fails else 0)
 
 
+def shards():
+    """Random circuits on the sharded engine (P = 2, 4, 8 segments on one
+    device: the multi-GPU exchange and relocation logic) against the oracle;
+    permutation-only circuits must match the unsharded engine bit for bit."""
+    from paper_2308_01999_b200.circuits import gen_qft, random_gate_sequence, to_gates
+    from paper_2308_01999_b200.shard import ShardedStateVector
+
+    cases = int(sys.argv[1])
+    rng = np.random.default_rng(20261019)
+    fails = []
+    t0 = time.time()
+    for c in range(cases):
+        n = int(rng.integers(6, 17))
+        dtype = (np.complex64, np.complex128)[c % 2]
+        P = int(2 ** rng.integers(1, 4))
+        gates = random_gate_sequence(n, 30, rng, max_arity=3) if c % 3 else to_gates(gen_qft(n))
+        sh = ShardedStateVector(n, [0] * P, dtype)
+        sh.run(gates)
+        got = sh.gather_logical()
+        sh.close()
+        want = O.run_circuit(gates, n)
+        try:
+            assert_state_close(got, want, dtype)
+        except AssertionError as e:
+            fails.append((c, n, np.dtype(dtype).name, P, str(e)[:200]))
+    print(f"shard fuzz: {cases} circuits in {time.time() - t0:.0f} s, {len(fails)} failures")
+    for f in fails[:20]:
+        print("FAIL", f)
+    sys.exit(1 if fails else 0)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[2] == "circuits":
         circuits()
+    elif len(sys.argv) > 2 and sys.argv[2] == "shards":
+        shards()
     else:
         main()
