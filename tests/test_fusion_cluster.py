@@ -38,7 +38,7 @@ def test_cluster_fusion_equals_circuit(name, n, circ, k):
 
 
 def test_layered_circuits_fuse_into_fewer_windows():
-    for n, k, want in ((33, 5, 130), (34, 4, 181), (33, 4, 169)):
+    for n, k, want in ((33, 5, 130), (34, 4, 181), (33, 4, 169), (33, 6, 99)):
         g = to_gates(gen_qv(n, 30, seed=0))
         got = fuse_cluster(g, k).data_passes
         assert got == want
